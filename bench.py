@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Himeno Jacobi on B200: GFLOPS + HBM roofline, e2e through the C ABI, GA evals/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs; north_star's headline grid): Himeno L
+(257 x 257 x 513, fp32), the best gene pattern's jacobi(nn): the device-resident
+time loop (gene 6; fused stencil with p/wrk2 rotation).  One *step* =
+one jacobi(nn) call, nn = 10 iterations.  Inputs (1.9 GB) exceed the 126 MB L2,
+so no flush is needed between steps.  GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
+
+* value      device-resident: K steps between CUDA events on the library's
+             stream, barrier + synchronize on both sides, max over ranks.
+* e2e        hp_jacobi_host (C ABI) with pinned HOST buffers: H2D of the 13
+             input arrays, the time loop, D2H of p and gosa -- per step.
+* roofline   dominant kernel = the stencil launch; achieved = 56 B/pt * N_int /
+             its CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline  the CPU oracle's jacobi on the same grid, all host threads.
+* ga         run_ga (pop 20 x gen 10, Himeno M, nn=3) with B200Evaluator on this
+             rank's GPU: fresh evaluations/s and generations/s.
+
+N > 1 (torchrun): each rank runs the full workload on its own GPU (replicas;
+DESIGN.md §Multi-GPU -- the slab decomposition is not wired into bench yet);
+scaling "weak".  --impl reference: rank 0 times the CPU reference path
+(oracle jacobi, OpenMP over all host cores); other ranks exit 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOP_PER_POINT = 34
+BYTES_STENCIL = 56
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        if self.path and os.path.exists(self.path):
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    return world, rank, local
+
+
+def cpu_baseline(size, seconds: float, threads: int) -> dict:
+    """CPU oracle jacobi on the same grid, bounded to ~`seconds` of work."""
+    from oracle import oracle
+    f = oracle.empty_fields(size.I, size.J, size.K)
+    oracle.initmt(f)
+    oracle.jacobi(f, 1, threads=threads)                # warm caches / first touch
+    iters, t0 = 0, time.perf_counter()
+    while True:
+        oracle.jacobi(f, 1, threads=threads)
+        iters += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or iters >= 50:
+            break
+    gf = FLOP_PER_POINT * size.interior_points * iters / el / 1e9
+    return {"value": gf, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"oracle jacobi on Himeno {size.name} ({size.I}x{size.J}x{size.K}), "
+                      f"{iters} iteration(s) after initmt, {threads} OpenMP threads, {el:.2f} s"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    from paper_2002_12115_b200.apps import himeno
+    size = himeno.size(args.size)
+    threads = oracle.max_threads()
+    f = oracle.empty_fields(size.I, size.J, size.K)
+    oracle.initmt(f)
+    for _ in range(args.warmup):
+        oracle.jacobi(f, 1, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.jacobi(f, 1, threads=threads)
+    el = time.perf_counter() - t0
+    value = FLOP_PER_POINT * size.interior_points * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": "Himeno GFLOPS", "value": value, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (Himeno initmt state)",
+        "config": {"workload": f"himeno_{size.name}_jacobi", "grid": [size.I, size.J, size.K],
+                   "nn_per_step": 1, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"oracle jacobi (C restatement of the program the reference "
+                                   f"compiles, gcc -O2, OpenMP {threads} threads), 1 iteration "
+                                   f"per step on Himeno {size.name}"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, seed: int) -> dict:
+    from paper_2002_12115_b200 import ga
+    from paper_2002_12115_b200.evaluator import B200Evaluator
+    with B200Evaluator(size_name, nn=nn, devices=[device]) as ev:
+        ev.measure((0,) * ev.gene_length)                  # context + first-touch warm-up
+        t0 = time.perf_counter()
+        res = ga.run_ga(ga.GAConfig(population=pop, generations=gens, rng_seed=seed),
+                        ev.gene_length, ev)
+        el = time.perf_counter() - t0
+        ok = sum(1 for r in res.records for i in r.individuals if i.eval_source == "fresh")
+    return {"size": size_name, "nn": nn, "population": pop, "generations": gens, "seed": seed,
+            "wall_s": el, "fresh_evals": res.evaluations, "valid_fresh": ok,
+            "evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
+            "best_genome": ga.genome_str(res.best.genome), "best_time_s": res.best.time_s}
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2002_12115_b200 import native as N
+    from paper_2002_12115_b200.apps import himeno
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    size = himeno.size(args.size)
+    nn, variant = args.nn, args.variant
+    flops_step = FLOP_PER_POINT * size.interior_points * nn
+    ctx = N.Context(local, size.I, size.J, size.K)
+    ctx.init_device()
+    for _ in range(args.warmup):
+        ctx.time_steps(1, nn, variant)
+
+    n0 = ctx.launch_count
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ms = ctx.time_steps(args.steps, nn, variant)
+        torch.cuda.synchronize()
+        barrier()
+    launches = ctx.launch_count - n0
+    clk = clocks.summary()
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = world * args.steps * flops_step / (ms_max / 1e3) / 1e9
+
+    # correctness of the timed state: gosa finite and positive
+    gosa = ctx.read_gosa(1)
+    assert gosa == gosa and gosa > 0, f"bad gosa {gosa}"
+
+    # dominant kernel (the stencil launch), CUDA events per launch
+    kt = ctx.time_jacobi(nn, variant)
+    peak, peak_src = peaks()
+    achieved = BYTES_STENCIL * size.interior_points / (kt.stencil_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("stencil_dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_stencil_3d (fused time loop)" if variant == 1 else "k_stencil_3d",
+                "bytes_per_point": BYTES_STENCIL, "points_per_launch": size.interior_points,
+                "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,
+                "peak_source": peak_src}
+
+    # e2e through the C ABI with pinned host buffers
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    host = {}
+    ctx.init_device()
+    import ctypes
+    pinned = []
+    nbytes = size.I * size.J * size.K * 4
+    for name in N.FIELDS:
+        ptr = ctx.lib.hp_host_alloc(nbytes)
+        if not ptr:
+            raise RuntimeError("pinned allocation failed")
+        pinned.append(ptr)
+        arr = np.ctypeslib.as_array((ctypes.c_float * (nbytes // 4)).from_address(ptr))
+        host[name] = arr.reshape(size.I, size.J, size.K)
+        host[name][...] = ctx.read_field(name, 1)
+    p_out = host["wrk2"]   # wrk2 is not an input; reuse its pinned buffer for p
+    ctx.jacobi_host(host, nn, variant, p_out)     # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.jacobi_host(host, nn, variant, p_out)
+    e2e_s = time.perf_counter() - t0
+    barrier()
+    for ptr in pinned:
+        ctx.lib.hp_host_free(ptr)
+    e2e_value = world * e2e_steps * flops_step / e2e_s / 1e9
+    e2e = {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": 13 * nbytes,
+           "d2h_bytes_per_step": nbytes + 8, "steps": e2e_steps,
+           "ms_per_step": e2e_s * 1e3 / e2e_steps, "path": "hp_jacobi_host (C ABI), pinned host"}
+
+    extra = {}
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+        extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
+    if rank == 0 and not args.no_ga:
+        extra["ga"] = ga_throughput(local, args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
+                                    args.ga_seed)
+    ctx.close()
+
+    if rank == 0:
+        line = {
+            "metric": "Himeno GFLOPS", "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Himeno initmt state, deterministic)",
+            "config": {"workload": f"himeno_{size.name}_jacobi", "grid": [size.I, size.J, size.K],
+                       "nn_per_step": nn, "pattern": "0000001000000 (device time loop)",
+                       "variant": "fused rotation" if variant == 1 else "stencil+copy",
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs 1.9 GB > 126 MB L2 (no flush)"},
+            "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "gosa": gosa,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", default="L")
+    ap.add_argument("--nn", type=int, default=10)
+    ap.add_argument("--variant", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-ga", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ga-size", default="M")
+    ap.add_argument("--ga-nn", type=int, default=3)
+    ap.add_argument("--ga-pop", type=int, default=20)
+    ap.add_argument("--ga-gens", type=int, default=10)
+    ap.add_argument("--ga-seed", type=int, default=0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

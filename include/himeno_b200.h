@@ -1,0 +1,218 @@
+/*
+ * himeno_b200.h -- C ABI of libhimeno_b200.so, the B200 fitness-evaluation engine.
+ *
+ * The reference evaluates one genome by emitting OpenACC C, compiling it and
+ * timing the process (acctuner/evaluators.py:178-222, ExternalEvaluator.measure
+ * -> _compile_and_run).  This library replaces that compile+run step: the
+ * Python evaluator lowers (genome, directive kinds, loop tree, TransferPlan)
+ * into an hp_schedule and one hp_run() call executes the Himeno program under
+ * that pattern -- gene=1 loops as sm_100a kernels, gene=0 loops as C++ host
+ * loops, plan entries as pinned host<->device transfers -- and reports the
+ * wall time the reference would have measured around the process
+ * (evaluators.py:207-214).
+ *
+ * Reference interface each entry point replaces:
+ *   hp_run          ExternalEvaluator.measure / _compile_and_run   evaluators.py:178-181, 190-222
+ *   hp_result.gosa  + samples: the program's stdout that
+ *                   ExternalEvaluator.run_for_output returns      evaluators.py:183-188
+ *   status codes    MeasuredTime.ok / timeout / failed             evaluators.py:28-46
+ *   hp_last_error   diagnostic text of MeasuredTime.failed / EvaluatorUnavailable
+ *                                                                   evaluators.py:204-205, 219-222
+ *   hp_create/hp_destroy  one device context per evaluator worker; the reference's
+ *                   max_concurrency thread pool (ga.py:222-230) leases one each.
+ *
+ * Conventions: plain C types only; all pointers are caller-owned and only
+ * read during the call; a context is NOT re-entrant, distinct contexts may be
+ * used concurrently from different threads (ctypes releases the GIL).
+ * Return codes: 0 ok; >0 pattern-level failure (maps to MeasuredTime.failed /
+ * timeout, the GA continues); <0 environment failure (maps to
+ * EvaluatorUnavailable, the run aborts).
+ */
+#ifndef HIMENO_B200_H
+#define HIMENO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+enum hp_status {
+  HP_OK = 0,
+  HP_FAIL_PATTERN = 1,   /* invalid pattern, e.g. nested compute construct      */
+  HP_FAIL_LAUNCH = 2,    /* kernel launch / execution error                      */
+  HP_TIMEOUT = 3,        /* watchdog (hp_schedule.timeout_s) expired             */
+  HP_FAIL_PRESENT = 4,   /* present assertion failed (data not on device)        */
+  HP_ERR_DEVICE = -1,    /* no device / CUDA context failure                     */
+  HP_ERR_ARG = -2,       /* bad argument (null pointer, wrong sizes)             */
+  HP_ERR_OOM = -3        /* device or pinned host allocation failed              */
+};
+
+/* ---- program description (Himeno, apps/himeno.py) ---------------------- */
+#define HP_NLOOPS 13     /* loop ids 0..12 in document order                    */
+#define HP_NFIELDS 14    /* fp32 arrays                                          */
+
+enum hp_field {          /* device/host fp32 arrays, each I*J*K               */
+  HP_F_P = 0, HP_F_BND, HP_F_WRK1, HP_F_WRK2,
+  HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3,
+  HP_F_B0, HP_F_B1, HP_F_B2,
+  HP_F_C0, HP_F_C1, HP_F_C2
+};
+
+enum hp_var {            /* plannable variables of the program (VarRefTable keys) */
+  HP_V_P = 0,            /* p                      -> HP_F_P                   */
+  HP_V_BND,              /* bnd                                                */
+  HP_V_WRK1,             /* wrk1                                               */
+  HP_V_WRK2,             /* wrk2                                               */
+  HP_V_A,                /* a[4]                   -> HP_F_A0..A3              */
+  HP_V_B,                /* b[3]                                               */
+  HP_V_C,                /* c[3]                                               */
+  HP_V_IMAX, HP_V_JMAX, HP_V_KMAX, HP_V_OMEGA,   /* global scalars             */
+  HP_V_NN,               /* jacobi:nn                                          */
+  HP_V_GOSA,             /* jacobi:gosa (carried in fp64)       */
+  HP_V_S0, HP_V_SS,      /* jacobi:s0, jacobi:ss (private in kernels)          */
+  HP_V_MAIN_GOSA,        /* main:gosa (never on device)                        */
+  HP_NVARS
+};
+
+enum hp_kind {           /* per-loop execution: gene 0 = host, else directive kind */
+  HP_K_HOST = 0,
+  HP_K_KERNELS = 1,      /* collapse the tight nest below the loop into one launch */
+  HP_K_PARALLEL_LOOP = 2,/* one gang per iteration of this loop, vector inside     */
+  HP_K_PLV = 3,          /* parallel loop vector: one gang, vector lanes only      */
+  HP_K_COVERED = 4       /* inside a device anchor (executed by the anchor)        */
+};
+
+enum hp_event_op {       /* data-manager events lowered from TransferPlan entries */
+  HP_EV_UPDATE_DEVICE = 1,  /* temp_region && into_device   : before each open  */
+  HP_EV_UPDATE_SELF = 2,    /* temp_region && out_of_device : after each close  */
+  HP_EV_DATA_ENTER = 3,     /* structured region enter, arg = copyin            */
+  HP_EV_DATA_EXIT = 4,      /* structured region exit,  arg = copyout           */
+  HP_EV_DECLARE = 5,        /* declare create (program lifetime), loop_id = -1  */
+  HP_EV_PRESENT = 6         /* present assertion at a covered anchor            */
+};
+
+enum hp_when { HP_BEFORE = 0, HP_AFTER = 1 };
+
+typedef struct hp_grid {
+  int32_t I, J, K;       /* static extents, k contiguous (RIKEN MIMAX/MJMAX/MKMAX) */
+} hp_grid;
+
+typedef struct hp_event {
+  int32_t loop_id;       /* statement the event is attached to (-1: program start) */
+  int32_t when;          /* hp_when                                                */
+  int32_t op;            /* hp_event_op                                            */
+  int32_t var;           /* hp_var                                                 */
+  int32_t arg;           /* copy flag for DATA_ENTER / DATA_EXIT                   */
+  int32_t entry;         /* index of the PlanEntry it came from (diagnostics)      */
+} hp_event;
+
+enum hp_flags {
+  HP_FLAG_COHERENCE_GUARD = 1,  /* skip transfers from a stale copy    */
+  HP_FLAG_FRESH_PROCESS = 2,    /* reset host arrays to static-zero before the run  */
+  HP_FLAG_POISON_DEVICE = 4,    /* fill device mirrors with NaN before the run      */
+  HP_FLAG_KERNEL_TIMING = 8,    /* CUDA events around every launch (slower)         */
+  HP_FLAG_GRAPH_TIME_LOOP = 16, /* replay the device time loop as a CUDA graph      */
+  HP_FLAG_FUSED_TIME_LOOP = 32  /* time loop: fused stencil with p/wrk2 rotation    */
+};
+
+typedef struct hp_schedule {
+  int32_t n_loops;                 /* must be HP_NLOOPS                            */
+  int32_t loop_kind[HP_NLOOPS];    /* hp_kind per loop id                          */
+  int32_t n_events;
+  const hp_event* events;          /* program order within one (loop, when) slot   */
+  int32_t nn;                      /* jacobi(nn) iteration count                   */
+  int32_t flags;                   /* hp_flags                                     */
+  double timeout_s;                /* watchdog; <= 0 disables                      */
+} hp_schedule;
+
+#define HP_MAX_SAMPLES 8
+
+typedef struct hp_result {
+  double wall_s;          /* host wall clock around the program run (the fitness time) */
+  double kernel_s;        /* sum of kernel durations (HP_FLAG_KERNEL_TIMING only)       */
+  double host_s;          /* time in host (gene=0) loop nests                           */
+  double xfer_s;          /* host time blocked in transfers                             */
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t n_h2d, n_d2h;            /* issued transfers                                 */
+  uint64_t n_skipped_stale;         /* plan transfers skipped by the coherence guard    */
+  uint64_t n_implicit;              /* implicit present_or_copy transfers               */
+  uint64_t n_launch;                /* kernels launched                                 */
+  uint64_t n_stale_reads;           /* compute read a copy older than the other side    */
+  double gosa;            /* main's printed gosa: host copy after jacobi returns    */
+  float samples[HP_MAX_SAMPLES];    /* main's printed p samples (host copy)         */
+  int32_t n_samples;
+  int32_t status;         /* hp_status                                              */
+  char diag[256];
+} hp_result;
+
+/* ---- library ------------------------------------------------------------ */
+int hp_abi_version(void);
+int hp_device_count(void);
+const char* hp_last_error(void);   /* thread-local message of the last failure */
+
+/* ---- context: one per device/worker --------------------------------------- */
+typedef struct hp_ctx hp_ctx;
+int hp_create(int device, const hp_grid* grid, int flags, hp_ctx** out);
+void hp_destroy(hp_ctx* ctx);
+void* hp_stream(hp_ctx* ctx);      /* the cudaStream_t every launch/copy uses */
+
+/* Set the p-sample points main prints (i,j,k triples); default: none. */
+int hp_set_samples(hp_ctx* ctx, int n, const int32_t* ijk);
+
+/* ---- fitness evaluation: run the program under one pattern ---------------- */
+int hp_run(hp_ctx* ctx, const hp_schedule* sched, hp_result* res);
+
+/* ---- field access (parity / e2e) ------------------------------------------ */
+/* side 0 = host copy (the program's static array), 1 = device mirror.
+ * dst/src hold I*J*K floats in the program's [i][j][k] layout. */
+int hp_read_field(hp_ctx* ctx, int field, int side, float* dst, size_t n);
+int hp_write_field(hp_ctx* ctx, int field, int side, const float* src, size_t n);
+int hp_read_gosa(hp_ctx* ctx, int side, double* out);
+
+/* ---- device-resident Jacobi (bench value / e2e) ----------------------------
+ * hp_jacobi_device: nn iterations of jacobi's loop body on the device mirrors,
+ * enqueued on hp_stream(ctx) without host synchronisation.  variant: 0 = the
+ * kernels selected for pattern 0000001000000 (stencil_3d + copy_3d),
+ * 1 = fused time loop (p/wrk2 rotation, copy nest elided, 56 B/pt).
+ * hp_jacobi_host: end-to-end offload of jacobi(nn) from host buffers: H2D of
+ * the 13 input fields (fields[HP_F_*], wrk2 ignored), the device loop, D2H of
+ * p into p_out and gosa into *gosa_out; synchronous.  Host buffers may be
+ * pageable or pinned (pinned is faster). */
+int hp_jacobi_device(hp_ctx* ctx, int nn, int variant);
+int hp_jacobi_host(hp_ctx* ctx, const float* const* fields, int nn, int variant,
+                   float* p_out, double* gosa_out);
+/* Initialise the device mirrors to the program's post-initmt state on device. */
+int hp_init_device(hp_ctx* ctx);
+/* Launch-level timing of the last hp_jacobi_device call region: the caller
+ * records its own events on hp_stream(); this helper reports the stream id's
+ * kernel count per iteration for the given variant. */
+int hp_launches_per_iteration(int variant);
+
+/* ---- device timing (bench.py) ----------------------------------------------
+ * hp_time_steps: CUDA events on hp_stream(ctx) around `steps` back-to-back
+ * hp_jacobi_device(nn, variant) calls; synchronous; *ms_out = elapsed ms.
+ * hp_time_jacobi: one jacobi(nn) call with events around every launch; reports
+ * the mean duration of the stencil launches and of the other launches. */
+typedef struct hp_kernel_times {
+  double total_ms;        /* first to last event of the call                 */
+  double stencil_ms;      /* mean duration of one stencil launch              */
+  double other_ms;        /* mean duration of the other launches (copies)     */
+  int32_t n_stencil, n_other;
+} hp_kernel_times;
+int hp_time_steps(hp_ctx* ctx, int steps, int nn, int variant, double* ms_out);
+int hp_time_jacobi(hp_ctx* ctx, int nn, int variant, hp_kernel_times* out);
+uint64_t hp_launch_count(hp_ctx* ctx);   /* kernels launched by this context so far */
+
+/* Pinned host buffers for callers without their own allocator (e2e inputs). */
+void* hp_host_alloc(size_t bytes);
+void hp_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIMENO_B200_H */

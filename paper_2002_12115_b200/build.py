@@ -1,0 +1,105 @@
+"""Build libhimeno_b200.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2002_12115_b200.build [--force] [--verbose]
+
+* kernels.cu   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
+               --fmad=false (bit-exact with the host loops / oracle)
+* executor.cpp g++ -O3 -ffp-contract=off (no FMA contraction on the host loops)
+* link         nvcc -shared -cudart static  ->  paper_2002_12115_b200/_native/
+
+The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
+Rebuilds only when a source or header is newer than the library.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT_DIR = PKG / "_native"
+LIB = OUT_DIR / "libhimeno_b200.so"
+INCLUDE = ROOT / "include"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _cuda_home() -> Path:
+    for cand in (os.environ.get("CUDA_HOME"), "/usr/local/cuda"):
+        if cand and (Path(cand) / "bin" / "nvcc").exists():
+            return Path(cand)
+    nvcc = shutil.which("nvcc")
+    if nvcc:
+        return Path(nvcc).resolve().parent.parent
+    raise RuntimeError("nvcc not found (set CUDA_HOME)")
+
+
+def _sources() -> list:
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    newest = max(p.stat().st_mtime for p in
+                 _sources() + sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h")) + [Path(__file__)])
+    return newest > LIB.stat().st_mtime
+
+
+def _run(cmd: list, verbose: bool) -> None:
+    if verbose:
+        print(" ".join(map(str, cmd)), flush=True)
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(map(str, cmd))}\n{proc.stdout}\n{proc.stderr}")
+    if verbose and (proc.stdout.strip() or proc.stderr.strip()):
+        print(proc.stdout + proc.stderr, flush=True)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale():
+        return LIB
+    cuda = _cuda_home()
+    nvcc = str(cuda / "bin" / "nvcc")
+    OUT_DIR.mkdir(exist_ok=True)
+    objs = []
+    inc = ["-I", str(INCLUDE), "-I", str(CSRC)]
+    for src in sorted(CSRC.glob("*.cu")):
+        obj = OUT_DIR / (src.stem + ".o")
+        _run([nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+              *inc, "-c", str(src), "-o", str(obj)], verbose)
+        objs.append(obj)
+    for src in sorted(CSRC.glob("*.cpp")):
+        obj = OUT_DIR / (src.stem + ".o")
+        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+              "-Wall", "-Wno-unused-function", "-I", str(cuda / "include"), *inc,
+              "-c", str(src), "-o", str(obj)], verbose)
+        objs.append(obj)
+    tmp = LIB.with_suffix(".so.tmp")
+    _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
+          "-Xlinker", "-soname=libhimeno_b200.so"], verbose)
+    os.replace(tmp, LIB)
+    for obj in objs:
+        obj.unlink(missing_ok=True)
+    return LIB
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args(argv)
+    lib = build(force=args.force, verbose=args.verbose)
+    print(lib)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

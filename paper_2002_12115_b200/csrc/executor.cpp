@@ -1,0 +1,1140 @@
+// Schedule executor + device data manager for the Himeno program (C ABI in
+// include/himeno_b200.h).
+//
+// One hp_run() = one execution of the program the reference would have
+// compiled and timed (acctuner/evaluators.py:190-222), under one gene pattern:
+//
+//   main:   imax = I-1; jmax = J-1; kmax = K-1; omega = 0.8      (host)
+//           initmt():  nest(0,1,2) zero, nest(3,4,5) coefficients
+//           gosa = jacobi(nn): loop 6 { gosa = 0; nest(7,8,9); nest(10,11,12) }
+//           print gosa and the p samples                          (host copies)
+//
+// Every loop statement is executed by `run_loop`: fire the plan events
+// attached before it, then either launch the device kernel variant selected
+// by its directive kind (gene = 1: the loop is an anchor), or iterate it on
+// the host (gene = 0) -- descending into children only when something below
+// needs it (a device anchor or an event), else running the whole sub-nest as
+// a tight C++ loop -- and fire the events attached after it.
+//
+// Data manager: every variable has a host and a
+// device copy with a write version each.  Plan events execute literally
+// (update device/self, structured data enter/exit with present_or_copy
+// reference counts, declare create); kernels touching arrays that are not
+// present get implicit present_or_copy around the launch (the per-kernel
+// copies the paper's batching removes).  With HP_FLAG_COHERENCE_GUARD a
+// transfer whose source copy is older than its destination is skipped and
+// counted (n_skipped_stale) instead of clobbering newer data.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "hp_internal.h"
+
+using namespace hp;
+
+// ------------------------------------------------------------------ errors
+
+static thread_local std::string g_last_error;
+
+static void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+extern "C" const char* hp_last_error(void) { return g_last_error.c_str(); }
+extern "C" int hp_abi_version(void) { return HP_ABI_VERSION; }
+
+extern "C" int hp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// --------------------------------------------------------- program tables
+
+namespace {
+
+enum { SLOT_BYTES = 8 };
+
+struct VarInfo {
+  const char* name;
+  int nfields;          // >0: array var made of fields [f0, f0 + nfields)
+  int f0;
+  int bytes;            // scalar size (0 for arrays)
+};
+
+const VarInfo kVars[HP_NVARS] = {
+    {"p", 1, HP_F_P, 0},        {"bnd", 1, HP_F_BND, 0},   {"wrk1", 1, HP_F_WRK1, 0},
+    {"wrk2", 1, HP_F_WRK2, 0},  {"a", 4, HP_F_A0, 0},      {"b", 3, HP_F_B0, 0},
+    {"c", 3, HP_F_C0, 0},       {"imax", 0, 0, 4},         {"jmax", 0, 0, 4},
+    {"kmax", 0, 0, 4},          {"omega", 0, 0, 4},        {"jacobi:nn", 0, 0, 4},
+    {"jacobi:gosa", 0, 0, 8},   {"jacobi:s0", 0, 0, 4},    {"jacobi:ss", 0, 0, 4},
+    {"main:gosa", 0, 0, 4}};
+
+// loop id -> nest and level; loop 6 is the time loop
+constexpr int kNestOf[HP_NLOOPS] = {NEST_INIT0, NEST_INIT0, NEST_INIT0, NEST_INIT1, NEST_INIT1,
+                                   NEST_INIT1, -1,         NEST_STENCIL, NEST_STENCIL,
+                                   NEST_STENCIL, NEST_COPY, NEST_COPY,   NEST_COPY};
+constexpr int kLevelOf[HP_NLOOPS] = {0, 1, 2, 0, 1, 2, -1, 0, 1, 2, 0, 1, 2};
+constexpr int kParentOf[HP_NLOOPS] = {-1, 0, 1, -1, 3, 4, -1, 6, 7, 8, 6, 10, 11};
+constexpr int kNestLoops[4][3] = {{0, 1, 2}, {3, 4, 5}, {7, 8, 9}, {10, 11, 12}};
+
+// variables each nest's body touches (reads, writes); scalars read by value
+struct NestVars { std::vector<int> arrays; std::vector<int> writes; bool gosa; };
+
+const NestVars& nest_vars(int nest) {
+  static const NestVars v[4] = {
+      {{HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C},
+       {HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C}, false},
+      {{HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C},
+       {HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C}, false},
+      {{HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_WRK2, HP_V_A, HP_V_B, HP_V_C}, {HP_V_WRK2}, true},
+      {{HP_V_P, HP_V_WRK2}, {HP_V_P}, false}};
+  return v[nest];
+}
+
+double now_s() {
+  using clk = std::chrono::steady_clock;
+  return std::chrono::duration<double>(clk::now().time_since_epoch()).count();
+}
+
+size_t round_up(size_t x, size_t q) { return (x + q - 1) / q * q; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+
+struct hp_ctx {
+  int device = 0;
+  int I = 0, J = 0, K = 0, P = 0;
+  size_t field_elems = 0;        // I*J*P
+  size_t field_stride = 0;       // slab offset between fields (2 MiB aligned)
+  cudaStream_t stream = nullptr;
+  float* slab = nullptr;         // HP_NFIELDS + 1 (rotation scratch) fields
+  DevFields dev{};
+  float* scratch = nullptr;      // rotation buffer for the fused time loop
+  float* host[HP_NFIELDS] = {};  // pinned [I][J][K]
+  unsigned char* hscal = nullptr;   // pinned scalar slots
+  unsigned char* dscal = nullptr;   // device scalar slots
+  double* partials = nullptr;
+  unsigned int* ticket = nullptr;
+  int capacity = 0;
+  std::vector<int32_t> samples;  // i,j,k triples
+  // per-run data-manager state
+  uint64_t clock = 0;
+  uint64_t host_ver[HP_NVARS] = {}, dev_ver[HP_NVARS] = {};
+  bool declared[HP_NVARS] = {};
+  int refcount[HP_NVARS] = {};
+  bool host_dirty[HP_NFIELDS] = {};  // written since the last fresh-process reset
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t launches = 0;         // kernels launched by this context (all entry points)
+
+  GosaSink sink() const {
+    GosaSink g;
+    g.slot = reinterpret_cast<double*>(dscal + HP_V_GOSA * SLOT_BYTES);
+    g.partials = partials;
+    g.ticket = ticket;
+    g.capacity = capacity;
+    return g;
+  }
+  HostFields hostf() const {
+    HostFields h;
+    for (int f = 0; f < HP_NFIELDS; ++f) h.f[f] = host[f];
+    h.I = I; h.J = J; h.K = K;
+    return h;
+  }
+  template <class T> T& hs(int v) { return *reinterpret_cast<T*>(hscal + v * SLOT_BYTES); }
+};
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? HP_ERR_OOM : HP_ERR_DEVICE;
+}
+
+#define CK(call, what)                         \
+  do {                                         \
+    cudaError_t e_ = (call);                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+extern "C" void hp_destroy(hp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->slab) cudaFree(c->slab);
+  if (c->dscal) cudaFree(c->dscal);
+  if (c->partials) cudaFree(c->partials);
+  if (c->ticket) cudaFree(c->ticket);
+  for (float* h : c->host)
+    if (h) cudaFreeHost(h);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+extern "C" int hp_create(int device, const hp_grid* grid, int flags, hp_ctx** out) {
+  (void)flags;
+  if (!grid || !out) {
+    set_error("hp_create: null argument");
+    return HP_ERR_ARG;
+  }
+  *out = nullptr;
+  if (grid->I < 4 || grid->J < 4 || grid->K < 4) {
+    set_error("hp_create: extents must be >= 4 (got %d x %d x %d)", grid->I, grid->J, grid->K);
+    return HP_ERR_ARG;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device available (%s)", cudaGetErrorString(e));
+    cudaGetLastError();
+    return HP_ERR_DEVICE;
+  }
+  if (device < 0 || device >= ndev) {
+    set_error("device %d out of range (have %d)", device, ndev);
+    return HP_ERR_ARG;
+  }
+  hp_ctx* c = new (std::nothrow) hp_ctx;
+  if (!c) {
+    set_error("out of host memory");
+    return HP_ERR_OOM;
+  }
+  c->device = device;
+  c->I = grid->I; c->J = grid->J; c->K = grid->K;
+  c->P = (int)round_up((size_t)c->K + 4, kRowAlign);
+  c->field_elems = (size_t)c->I * c->J * c->P;
+  c->field_stride = round_up(c->field_elems, (size_t)1 << 19);  // 2 MiB of floats
+  int rc = HP_OK;
+  auto fail = [&](int code) { hp_destroy(c); return code; };
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(cuda_fail(e, "cudaSetDevice"));
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaStreamCreate"));
+  const size_t slab_elems = c->field_stride * (HP_NFIELDS + 1);
+  if ((e = cudaMalloc(&c->slab, slab_elems * sizeof(float))) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMalloc(field slab)"));
+  c->dev.I = c->I; c->dev.J = c->J; c->dev.K = c->K; c->dev.P = c->P;
+  for (int f = 0; f < HP_NFIELDS; ++f) c->dev.f[f] = c->slab + (size_t)f * c->field_stride;
+  c->scratch = c->slab + (size_t)HP_NFIELDS * c->field_stride;
+  const size_t host_bytes = (size_t)c->I * c->J * c->K * sizeof(float);
+  for (int f = 0; f < HP_NFIELDS; ++f) {
+    if ((e = cudaHostAlloc(&c->host[f], host_bytes, cudaHostAllocPortable)) != cudaSuccess)
+      return fail(cuda_fail(e, "cudaHostAlloc(host field)"));
+    memset(c->host[f], 0, host_bytes);
+  }
+  if ((e = cudaHostAlloc(&c->hscal, HP_NVARS * SLOT_BYTES, cudaHostAllocPortable)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaHostAlloc(scalars)"));
+  memset(c->hscal, 0, HP_NVARS * SLOT_BYTES);
+  if ((e = cudaMalloc(&c->dscal, HP_NVARS * SLOT_BYTES)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMalloc(scalars)"));
+  c->capacity = gosa_capacity_needed(c->dev);
+  if ((e = cudaMalloc(&c->partials, (size_t)c->capacity * sizeof(double))) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMalloc(partials)"));
+  if ((e = cudaMalloc(&c->ticket, sizeof(unsigned int))) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMalloc(ticket)"));
+  cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream);
+  cudaMemsetAsync(c->dscal, 0, HP_NVARS * SLOT_BYTES, c->stream);
+  cudaMemsetAsync(c->slab, 0, slab_elems * sizeof(float), c->stream);
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess)
+    return fail(cuda_fail(e, "context init"));
+  (void)rc;
+  *out = c;
+  return HP_OK;
+}
+
+extern "C" void* hp_stream(hp_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+extern "C" int hp_set_samples(hp_ctx* c, int n, const int32_t* ijk) {
+  if (!c || n < 0 || n > HP_MAX_SAMPLES || (n && !ijk)) {
+    set_error("hp_set_samples: bad arguments");
+    return HP_ERR_ARG;
+  }
+  for (int s = 0; s < n; ++s) {
+    if (ijk[3 * s] < 0 || ijk[3 * s] >= c->I || ijk[3 * s + 1] < 0 || ijk[3 * s + 1] >= c->J ||
+        ijk[3 * s + 2] < 0 || ijk[3 * s + 2] >= c->K) {
+      set_error("hp_set_samples: sample %d out of range", s);
+      return HP_ERR_ARG;
+    }
+  }
+  c->samples.assign(ijk, ijk + 3 * n);
+  return HP_OK;
+}
+
+// ------------------------------------------------------------- host loops
+// Same expression order as the C program; built with -ffp-contract=off so
+// every product and sum rounds separately, exactly like the kernels.
+
+static void host_init0(const HostFields& H, const Box& b) {
+  for (int i = b.i0; i < b.i1; ++i)
+    for (int j = b.j0; j < b.j1; ++j)
+      for (int k = b.k0; k < b.k1; ++k) {
+        const size_t c = H.at(i, j, k);
+        for (int f = 0; f < HP_NFIELDS; ++f)
+          if (f != HP_F_WRK2) H.f[f][c] = 0.0f;
+      }
+}
+
+static void host_init1(const HostFields& H, const Box& b, int imax) {
+  const float a3 = (float)(1.0 / 6.0);
+  for (int i = b.i0; i < b.i1; ++i) {
+    const float pv = (float)(i * i) / (float)((imax - 1) * (imax - 1));
+    for (int j = b.j0; j < b.j1; ++j)
+      for (int k = b.k0; k < b.k1; ++k) {
+        const size_t c = H.at(i, j, k);
+        H.f[HP_F_A0][c] = 1.0f; H.f[HP_F_A1][c] = 1.0f; H.f[HP_F_A2][c] = 1.0f;
+        H.f[HP_F_A3][c] = a3;
+        H.f[HP_F_B0][c] = 0.0f; H.f[HP_F_B1][c] = 0.0f; H.f[HP_F_B2][c] = 0.0f;
+        H.f[HP_F_C0][c] = 1.0f; H.f[HP_F_C1][c] = 1.0f; H.f[HP_F_C2][c] = 1.0f;
+        H.f[HP_F_P][c] = pv;
+        H.f[HP_F_WRK1][c] = 0.0f;
+        H.f[HP_F_BND][c] = 1.0f;
+      }
+  }
+}
+
+static double host_stencil(const HostFields& H, const Box& b, float omega) {
+  const float* p = H.f[HP_F_P];
+  const float *a0 = H.f[HP_F_A0], *a1 = H.f[HP_F_A1], *a2 = H.f[HP_F_A2], *a3 = H.f[HP_F_A3];
+  const float *b0 = H.f[HP_F_B0], *b1 = H.f[HP_F_B1], *b2 = H.f[HP_F_B2];
+  const float *c0 = H.f[HP_F_C0], *c1 = H.f[HP_F_C1], *c2 = H.f[HP_F_C2];
+  const float *wrk1 = H.f[HP_F_WRK1], *bnd = H.f[HP_F_BND];
+  float* wrk2 = H.f[HP_F_WRK2];
+  const size_t R = (size_t)H.K, L = (size_t)H.J * H.K;
+  double acc = 0.0;
+  for (int i = b.i0; i < b.i1; ++i)
+    for (int j = b.j0; j < b.j1; ++j)
+      for (int k = b.k0; k < b.k1; ++k) {
+        const size_t c = H.at(i, j, k);
+        const float s0 = a0[c] * p[c + L] + a1[c] * p[c + R] + a2[c] * p[c + 1] +
+                         b0[c] * (p[c + L + R] - p[c + L - R] - p[c - L + R] + p[c - L - R]) +
+                         b1[c] * (p[c + R + 1] - p[c - R + 1] - p[c + R - 1] + p[c - R - 1]) +
+                         b2[c] * (p[c + L + 1] - p[c - L + 1] - p[c + L - 1] + p[c - L - 1]) +
+                         c0[c] * p[c - L] + c1[c] * p[c - R] + c2[c] * p[c - 1] + wrk1[c];
+        const float ss = (s0 * a3[c] - p[c]) * bnd[c];
+        const float t = ss * ss;
+        acc += (double)t;
+        wrk2[c] = p[c] + omega * ss;
+      }
+  return acc;
+}
+
+static void host_copy(const HostFields& H, const Box& b) {
+  for (int i = b.i0; i < b.i1; ++i)
+    for (int j = b.j0; j < b.j1; ++j) {
+      const size_t c = H.at(i, j, b.k0);
+      if (b.k1 > b.k0)
+        memcpy(H.f[HP_F_P] + c, H.f[HP_F_WRK2] + c, (size_t)(b.k1 - b.k0) * sizeof(float));
+    }
+}
+
+// ----------------------------------------------------------------- runner
+
+namespace {
+
+struct Runner {
+  hp_ctx* C;
+  const hp_schedule* S;
+  hp_result* R;
+  std::vector<const hp_event*> before[HP_NLOOPS], after[HP_NLOOPS];
+  bool busy_below[HP_NLOOPS] = {};   // device anchor or event strictly inside
+  double t_start = 0, deadline = 0;
+  bool guard = true;
+  bool pending_h2d = false;
+  int status = HP_OK;
+  char diag[256] = {0};
+
+  // --- helpers ---------------------------------------------------------------
+  bool failed() const { return status != HP_OK; }
+  void fail(int code, const char* fmt, ...) {
+    if (status != HP_OK) return;
+    status = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(diag, sizeof diag, fmt, ap);
+    va_end(ap);
+  }
+  bool check_time() {
+    if (deadline > 0 && now_s() > deadline) {
+      fail(HP_TIMEOUT, "watchdog: run exceeded %.1f s", S->timeout_s);
+      return false;
+    }
+    return true;
+  }
+  bool cuda_ok(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return true;
+    fail(HP_FAIL_LAUNCH, "%s: %s", what, cudaGetErrorString(e));
+    return false;
+  }
+  int kind(int loop) const { return S->loop_kind[loop]; }
+  bool on_device(int loop) const {
+    const int k = kind(loop);
+    return k == HP_K_KERNELS || k == HP_K_PARALLEL_LOOP || k == HP_K_PLV;
+  }
+  bool present(int v) const { return C->declared[v] || C->refcount[v] > 0; }
+  void host_write(int v) { C->host_ver[v] = ++C->clock; mark_host_dirty(v); }
+  void dev_write(int v) { C->dev_ver[v] = ++C->clock; }
+  void host_read(int v) { if (C->host_ver[v] < C->dev_ver[v]) R->n_stale_reads++; }
+  void dev_read(int v) { if (C->dev_ver[v] < C->host_ver[v]) R->n_stale_reads++; }
+  void mark_host_dirty(int v) {
+    const VarInfo& vi = kVars[v];
+    for (int f = 0; f < vi.nfields; ++f) C->host_dirty[vi.f0 + f] = true;
+  }
+
+  // --- transfers ---------------------------------------------------------------
+  void sync_pending() {
+    if (pending_h2d) {
+      const double t0 = now_s();
+      cuda_ok(cudaStreamSynchronize(C->stream), "sync before host loop");
+      R->xfer_s += now_s() - t0;
+      pending_h2d = false;
+    }
+  }
+  void h2d(int v, bool implicit) {
+    if (failed()) return;
+    if (guard && C->host_ver[v] < C->dev_ver[v]) {
+      R->n_skipped_stale++;
+      return;
+    }
+    const VarInfo& vi = kVars[v];
+    const double t0 = now_s();
+    if (vi.nfields) {
+      for (int f = 0; f < vi.nfields; ++f) {
+        const int fid = vi.f0 + f;
+        if (!cuda_ok(cudaMemcpy2DAsync(C->dev.f[fid], (size_t)C->P * sizeof(float), C->host[fid],
+                                       (size_t)C->K * sizeof(float), (size_t)C->K * sizeof(float),
+                                       (size_t)C->I * C->J, cudaMemcpyHostToDevice, C->stream),
+                     "update device"))
+          return;
+        R->h2d_bytes += (uint64_t)C->I * C->J * C->K * sizeof(float);
+        R->n_h2d++;
+      }
+    } else {
+      if (!cuda_ok(cudaMemcpyAsync(C->dscal + v * SLOT_BYTES, C->hscal + v * SLOT_BYTES,
+                                   (size_t)vi.bytes, cudaMemcpyHostToDevice, C->stream),
+                   "update device (scalar)"))
+        return;
+      R->h2d_bytes += (uint64_t)vi.bytes;
+      R->n_h2d++;
+    }
+    if (implicit) R->n_implicit++;
+    pending_h2d = true;
+    R->xfer_s += now_s() - t0;
+    C->dev_ver[v] = C->host_ver[v];
+  }
+  void d2h(int v, bool implicit) {
+    if (failed()) return;
+    if (guard && C->dev_ver[v] < C->host_ver[v]) {
+      R->n_skipped_stale++;
+      return;
+    }
+    const VarInfo& vi = kVars[v];
+    const double t0 = now_s();
+    if (vi.nfields) {
+      for (int f = 0; f < vi.nfields; ++f) {
+        const int fid = vi.f0 + f;
+        if (!cuda_ok(cudaMemcpy2DAsync(C->host[fid], (size_t)C->K * sizeof(float), C->dev.f[fid],
+                                       (size_t)C->P * sizeof(float), (size_t)C->K * sizeof(float),
+                                       (size_t)C->I * C->J, cudaMemcpyDeviceToHost, C->stream),
+                     "update self"))
+          return;
+        R->d2h_bytes += (uint64_t)C->I * C->J * C->K * sizeof(float);
+        R->n_d2h++;
+      }
+      mark_host_dirty(v);
+    } else {
+      if (!cuda_ok(cudaMemcpyAsync(C->hscal + v * SLOT_BYTES, C->dscal + v * SLOT_BYTES,
+                                   (size_t)vi.bytes, cudaMemcpyDeviceToHost, C->stream),
+                   "update self (scalar)"))
+        return;
+      R->d2h_bytes += (uint64_t)vi.bytes;
+      R->n_d2h++;
+    }
+    if (implicit) R->n_implicit++;
+    cuda_ok(cudaStreamSynchronize(C->stream), "update self (sync)");
+    pending_h2d = false;
+    R->xfer_s += now_s() - t0;
+    C->host_ver[v] = C->dev_ver[v];
+  }
+
+  // --- plan events ---------------------------------------------------------------
+  void fire(const hp_event* e) {
+    if (failed()) return;
+    const int v = e->var;
+    switch (e->op) {
+      case HP_EV_DECLARE:
+        C->declared[v] = true;
+        break;
+      case HP_EV_UPDATE_DEVICE:
+        h2d(v, false);
+        break;
+      case HP_EV_UPDATE_SELF:
+        d2h(v, false);
+        break;
+      case HP_EV_DATA_ENTER:
+        if (present(v)) {
+          if (!C->declared[v]) C->refcount[v]++;
+        } else {
+          C->refcount[v] = 1;
+          if (e->arg) h2d(v, false);
+        }
+        break;
+      case HP_EV_DATA_EXIT:
+        if (C->declared[v]) break;
+        if (C->refcount[v] > 0 && --C->refcount[v] == 0 && e->arg) d2h(v, false);
+        break;
+      case HP_EV_PRESENT:
+        if (!present(v))
+          fail(HP_FAIL_PRESENT, "present(%s) failed at loop %d: data not on device",
+               kVars[v].name, e->loop_id);
+        break;
+      default:
+        fail(HP_FAIL_PATTERN, "unknown event op %d", e->op);
+    }
+  }
+  void fire_all(const std::vector<const hp_event*>& evs) {
+    for (const hp_event* e : evs) fire(e);
+  }
+
+  // --- kernel launches ---------------------------------------------------------
+  LaunchArgs args(int reset) const {
+    LaunchArgs a;
+    a.imax = C->hs<int>(HP_V_IMAX);
+    a.jmax = C->hs<int>(HP_V_JMAX);
+    a.kmax = C->hs<int>(HP_V_KMAX);
+    a.omega = C->hs<float>(HP_V_OMEGA);
+    a.gosa_reset = reset;
+    return a;
+  }
+
+  // implicit present_or_copy for arrays (and the gosa reduction scalar)
+  void implicit_vars(int nest, std::vector<int>& out) const {
+    out.clear();
+    const NestVars& nv = nest_vars(nest);
+    for (int v : nv.arrays)
+      if (!present(v)) out.push_back(v);
+    if (nv.gosa && !present(HP_V_GOSA)) out.push_back(HP_V_GOSA);
+  }
+
+  void note_device_access(int nest) {
+    const NestVars& nv = nest_vars(nest);
+    for (int v : nv.arrays) {
+      bool w = std::find(nv.writes.begin(), nv.writes.end(), v) != nv.writes.end();
+      bool r = !(nest == NEST_INIT0 || nest == NEST_INIT1) && !(nest == NEST_STENCIL && v == HP_V_WRK2) &&
+               !(nest == NEST_COPY && v == HP_V_P);
+      if (r) dev_read(v);
+      if (w) dev_write(v);
+    }
+    if (nv.gosa) {
+      dev_read(HP_V_GOSA);
+      dev_write(HP_V_GOSA);
+    }
+  }
+
+  void launch(int nest, Mapping map, const Box& b, bool full_tuned) {
+    if (failed()) return;
+    std::vector<int> imp;
+    implicit_vars(nest, imp);
+    for (int v : imp) h2d(v, true);
+    if (failed()) return;
+    note_device_access(nest);
+    const LaunchArgs a = args(0);
+    int n;
+    if (full_tuned && map == MAP_COLLAPSE && nest == NEST_STENCIL)
+      n = launch_stencil_3d(C->dev, a, C->sink(), C->stream);
+    else if (full_tuned && map == MAP_COLLAPSE && nest == NEST_COPY)
+      n = launch_copy_3d(C->dev, a, C->stream);
+    else
+      n = launch_nest((Nest)nest, map, C->dev, b, a, C->sink(), C->stream);
+    if (n < 0) {
+      cudaError_t e = cudaGetLastError();
+      fail(HP_FAIL_LAUNCH, "launch of nest %d failed: %s", nest, cudaGetErrorString(e));
+      return;
+    }
+    R->n_launch += (uint64_t)n;
+    C->launches += (uint64_t)n;
+    for (int v : imp) d2h(v, true);
+  }
+
+  // --- nests ---------------------------------------------------------------------
+  Box nest_box(int nest) const {
+    const int imax = C->hs<int>(HP_V_IMAX), jmax = C->hs<int>(HP_V_JMAX),
+              kmax = C->hs<int>(HP_V_KMAX);
+    switch (nest) {
+      case NEST_INIT0: return Box{0, C->I, 0, C->J, 0, C->K};
+      case NEST_INIT1: return Box{0, imax, 0, jmax, 0, kmax};
+      default: return Box{1, imax - 1, 1, jmax - 1, 1, kmax - 1};
+    }
+  }
+
+  void host_nest(int nest, const Box& b) {
+    if (failed()) return;
+    sync_pending();
+    const double t0 = now_s();
+    const HostFields H = C->hostf();
+    const NestVars& nv = nest_vars(nest);
+    if (nest == NEST_STENCIL || nest == NEST_COPY)
+      for (int v : nv.arrays)
+        if (!(nest == NEST_STENCIL && v == HP_V_WRK2) && !(nest == NEST_COPY && v == HP_V_P))
+          host_read(v);
+    switch (nest) {
+      case NEST_INIT0: host_init0(H, b); break;
+      case NEST_INIT1: host_init1(H, b, C->hs<int>(HP_V_IMAX)); break;
+      case NEST_STENCIL: {
+        host_read(HP_V_GOSA);
+        C->hs<double>(HP_V_GOSA) += host_stencil(H, b, C->hs<float>(HP_V_OMEGA));
+        host_write(HP_V_GOSA);
+        break;
+      }
+      default: host_copy(H, b); break;
+    }
+    for (int v : nv.writes) host_write(v);
+    R->host_s += now_s() - t0;
+  }
+
+  Mapping mapping(int loop) const {
+    switch (kind(loop)) {
+      case HP_K_PARALLEL_LOOP: return MAP_GANG;
+      case HP_K_PLV: return MAP_VECTOR;
+      default: return MAP_COLLAPSE;
+    }
+  }
+
+  // Execute loop `level` of `nest` with outer indices fixed in `b`.
+  void run_level(int nest, int level, Box b) {
+    if (failed()) return;
+    const int loop = kNestLoops[nest][level];
+    fire_all(before[loop]);
+    if (on_device(loop)) {
+      launch(nest, mapping(loop), b, level == 0);
+    } else if (level < 2 && busy_below[loop]) {
+      const int lo = level == 0 ? b.i0 : b.j0, hi = level == 0 ? b.i1 : b.j1;
+      for (int x = lo; x < hi && !failed(); ++x) {
+        Box inner = b;
+        if (level == 0) { inner.i0 = x; inner.i1 = x + 1; }
+        else { inner.j0 = x; inner.j1 = x + 1; }
+        run_level(nest, level + 1, inner);
+        if (level == 0) check_time();
+      }
+    } else {
+      host_nest(nest, b);
+      check_time();
+    }
+    fire_all(after[loop]);
+  }
+
+  void run_nest(int nest) { run_level(nest, 0, nest_box(nest)); }
+
+  // device-resident time loop (gene 6 = 1)
+  void device_time_loop() {
+    if (failed()) return;
+    // implicit copies for everything the loop body touches
+    std::vector<int> imp, tmp;
+    implicit_vars(NEST_STENCIL, tmp);
+    imp = tmp;
+    implicit_vars(NEST_COPY, tmp);
+    for (int v : tmp)
+      if (std::find(imp.begin(), imp.end(), v) == imp.end()) imp.push_back(v);
+    if (!present(HP_V_GOSA) && std::find(imp.begin(), imp.end(), HP_V_GOSA) == imp.end())
+      imp.push_back(HP_V_GOSA);
+    for (int v : imp) h2d(v, true);
+    if (failed()) return;
+    const int nn = C->hs<int>(HP_V_NN);
+    const int k6 = kind(6);
+    const bool fused = (S->flags & HP_FLAG_FUSED_TIME_LOOP) && k6 != HP_K_PLV;
+    for (int v : {HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C}) dev_read(v);
+    int n = 0;
+    if (nn > 0) {
+      if (fused) {
+        n = time_loop_fused(C, nn, args(1));
+      } else {
+        const Box bs = nest_box(NEST_STENCIL);
+        for (int it = 0; it < nn && n >= 0; ++it) {
+          const LaunchArgs a = args(1);
+          int r1, r2;
+          if (k6 == HP_K_PLV) {
+            r1 = launch_nest(NEST_STENCIL, MAP_VECTOR, C->dev, bs, a, C->sink(), C->stream);
+            r2 = launch_nest(NEST_COPY, MAP_VECTOR, C->dev, bs, a, C->sink(), C->stream);
+          } else {
+            r1 = launch_stencil_3d(C->dev, a, C->sink(), C->stream);
+            r2 = launch_copy_3d(C->dev, a, C->stream);
+          }
+          n = (r1 < 0 || r2 < 0) ? -1 : n + r1 + r2;
+        }
+      }
+    }
+    if (n < 0) {
+      fail(HP_FAIL_LAUNCH, "time-loop launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return;
+    }
+    R->n_launch += (uint64_t)n;
+    C->launches += (uint64_t)n;
+    if (nn > 0) {
+      dev_write(HP_V_WRK2);
+      dev_write(HP_V_P);
+      dev_write(HP_V_GOSA);
+    }
+    for (int v : imp) d2h(v, true);
+  }
+
+ public:
+  static int time_loop_fused(hp_ctx* c, int nn, const LaunchArgs& a) {
+    // p -> scratch -> p ... ; faces of scratch mirror p's; final interior goes
+    // to p (if it ended in scratch) and to wrk2.
+    float* bufs[2] = {c->dev.f[HP_F_P], c->scratch};
+    int n = 0, r;
+    if ((r = launch_copy_halo(c->dev, bufs[0], bufs[1], a.imax, a.jmax, a.kmax, c->stream)) < 0)
+      return -1;
+    n += r;
+    for (int it = 0; it < nn; ++it) {
+      if ((r = launch_stencil_rotate(c->dev, bufs[it & 1], bufs[(it + 1) & 1], a, c->sink(),
+                                     c->stream)) < 0)
+        return -1;
+      n += r;
+    }
+    float* last = bufs[nn & 1];
+    if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a.imax, a.jmax,
+                                         a.kmax, c->stream)) < 0)
+      return -1;
+    n += r;
+    if (last != c->dev.f[HP_F_P]) {
+      if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a.imax, a.jmax,
+                                           a.kmax, c->stream)) < 0)
+        return -1;
+      n += r;
+    }
+    return n;
+  }
+
+  void run_time_loop() {
+    fire_all(before[6]);
+    if (on_device(6)) {
+      device_time_loop();
+    } else {
+      const int nn = C->hs<int>(HP_V_NN);
+      for (int it = 0; it < nn && !failed(); ++it) {
+        C->hs<double>(HP_V_GOSA) = 0.0;  // gosa = 0.0;  (host statement in loop 6)
+        host_write(HP_V_GOSA);
+        run_nest(NEST_STENCIL);
+        run_nest(NEST_COPY);
+        check_time();
+      }
+    }
+    fire_all(after[6]);
+  }
+
+  // --- setup -------------------------------------------------------------------
+  int prepare() {
+    if (S->n_loops != HP_NLOOPS) {
+      set_error("schedule has %d loops, program has %d", S->n_loops, HP_NLOOPS);
+      return HP_ERR_ARG;
+    }
+    if (S->n_events < 0 || (S->n_events > 0 && !S->events)) {
+      set_error("schedule events missing");
+      return HP_ERR_ARG;
+    }
+    for (int l = 0; l < HP_NLOOPS; ++l)
+      if (S->loop_kind[l] < HP_K_HOST || S->loop_kind[l] > HP_K_COVERED) {
+        set_error("loop %d: bad kind %d", l, S->loop_kind[l]);
+        return HP_ERR_ARG;
+      }
+    // nested compute constructs: reject (reference: compile failure -> penalty)
+    for (int l = 0; l < HP_NLOOPS; ++l) {
+      if (!on_device(l)) continue;
+      for (int a = kParentOf[l]; a >= 0; a = kParentOf[a])
+        if (on_device(a)) {
+          fail(HP_FAIL_PATTERN, "nested compute construct: loop %d inside device loop %d", l, a);
+          return HP_OK;
+        }
+    }
+    for (int n = 0; n < S->n_events; ++n) {
+      const hp_event* e = &S->events[n];
+      if (e->var < 0 || e->var >= HP_NVARS) {
+        set_error("event %d: bad var %d", n, e->var);
+        return HP_ERR_ARG;
+      }
+      if (e->op == HP_EV_DECLARE) continue;
+      if (e->loop_id < 0 || e->loop_id >= HP_NLOOPS) {
+        set_error("event %d: bad loop %d", n, e->loop_id);
+        return HP_ERR_ARG;
+      }
+      (e->when == HP_BEFORE ? before : after)[e->loop_id].push_back(e);
+      for (int a = kParentOf[e->loop_id]; a >= 0; a = kParentOf[a]) busy_below[a] = true;
+    }
+    for (int l = 0; l < HP_NLOOPS; ++l)
+      if (on_device(l))
+        for (int a = kParentOf[l]; a >= 0; a = kParentOf[a]) busy_below[a] = true;
+    // emitter stacking order: update device (10) < data (20) < present (30);
+    // after a statement: data exit / brace (60) < update self (90)
+    auto rank = [](const hp_event* e) {
+      switch (e->op) {
+        case HP_EV_UPDATE_DEVICE: return 10;
+        case HP_EV_DATA_ENTER: return 20;
+        case HP_EV_PRESENT: return 30;
+        case HP_EV_DATA_EXIT: return 60;
+        default: return 90;
+      }
+    };
+    for (int l = 0; l < HP_NLOOPS; ++l) {
+      std::stable_sort(before[l].begin(), before[l].end(),
+                       [&](const hp_event* x, const hp_event* y) { return rank(x) < rank(y); });
+      std::stable_sort(after[l].begin(), after[l].end(),
+                       [&](const hp_event* x, const hp_event* y) { return rank(x) < rank(y); });
+    }
+    return HP_OK;
+  }
+
+  void reset_state() {
+    C->clock = 1;
+    for (int v = 0; v < HP_NVARS; ++v) {
+      C->host_ver[v] = 1;   // static storage / declarations: host copy is defined
+      C->dev_ver[v] = 0;    // fresh device memory: undefined
+      C->declared[v] = false;
+      C->refcount[v] = 0;
+    }
+    memset(C->hscal, 0, HP_NVARS * SLOT_BYTES);
+  }
+
+  void program() {
+    // main: imax = I-1; jmax = J-1; kmax = K-1; omega = 0.8;
+    C->hs<int>(HP_V_IMAX) = C->I - 1; host_write(HP_V_IMAX);
+    C->hs<int>(HP_V_JMAX) = C->J - 1; host_write(HP_V_JMAX);
+    C->hs<int>(HP_V_KMAX) = C->K - 1; host_write(HP_V_KMAX);
+    C->hs<float>(HP_V_OMEGA) = 0.8f; host_write(HP_V_OMEGA);
+    for (int n = 0; n < S->n_events; ++n)
+      if (S->events[n].op == HP_EV_DECLARE) fire(&S->events[n]);
+    // initmt()
+    run_nest(NEST_INIT0);
+    run_nest(NEST_INIT1);
+    // gosa = jacobi(nn)
+    C->hs<int>(HP_V_NN) = S->nn; host_write(HP_V_NN);
+    run_time_loop();
+    sync_pending();
+    if (!failed()) cuda_ok(cudaStreamSynchronize(C->stream), "program end");
+    // main:gosa = jacobi's return value (host copy); printed with the p samples
+    host_read(HP_V_GOSA);
+    R->gosa = C->hs<double>(HP_V_GOSA);
+    host_read(HP_V_P);
+    const int ns = (int)C->samples.size() / 3;
+    R->n_samples = ns;
+    for (int s = 0; s < ns; ++s)
+      R->samples[s] = C->host[HP_F_P][C->hostf().at(C->samples[3 * s], C->samples[3 * s + 1],
+                                                   C->samples[3 * s + 2])];
+  }
+};
+
+}  // namespace
+
+extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
+  if (!c || !s || !r) {
+    set_error("hp_run: null argument");
+    return HP_ERR_ARG;
+  }
+  memset(r, 0, sizeof *r);
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  Runner run;
+  run.C = c;
+  run.S = s;
+  run.R = r;
+  run.guard = (s->flags & HP_FLAG_COHERENCE_GUARD) != 0;
+  int rc = run.prepare();
+  if (rc != HP_OK) return rc;
+  if (run.failed()) {  // rejected pattern: nothing executes
+    r->status = run.status;
+    memcpy(r->diag, run.diag, sizeof r->diag);
+    set_error("%s", run.diag);
+    return run.status;
+  }
+  // fresh process: static arrays zero, device memory undefined (not timed)
+  if (s->flags & HP_FLAG_FRESH_PROCESS) {
+    const size_t bytes = (size_t)c->I * c->J * c->K * sizeof(float);
+    for (int f = 0; f < HP_NFIELDS; ++f)
+      if (c->host_dirty[f]) {
+        memset(c->host[f], 0, bytes);
+        c->host_dirty[f] = false;
+      }
+  }
+  if (s->flags & HP_FLAG_POISON_DEVICE) {
+    if (launch_fill(c->slab, c->field_stride * (HP_NFIELDS + 1), nanf(""), c->stream) < 0)
+      return cuda_fail(cudaGetLastError(), "poison");
+  }
+  cudaMemsetAsync(c->dscal, 0xff, HP_NVARS * SLOT_BYTES, c->stream);
+  e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "pre-run sync");
+  run.reset_state();
+
+  run.t_start = now_s();
+  run.deadline = s->timeout_s > 0 ? run.t_start + s->timeout_s : 0;
+  run.program();
+  if (run.status == HP_TIMEOUT || run.status == HP_FAIL_LAUNCH) cudaStreamSynchronize(c->stream);
+  r->wall_s = now_s() - run.t_start;
+  // a sticky device error (illegal address, ...) poisons the context
+  e = cudaGetLastError();
+  if (e != cudaSuccess && run.status == HP_OK)
+    run.fail(HP_FAIL_LAUNCH, "device error: %s", cudaGetErrorString(e));
+  r->status = run.status;
+  memcpy(r->diag, run.diag, sizeof r->diag);
+  if (run.status != HP_OK) set_error("%s", run.diag);
+  return run.status;
+}
+
+// --------------------------------------------------------- field access
+
+extern "C" int hp_read_field(hp_ctx* c, int field, int side, float* dst, size_t n) {
+  if (!c || !dst || field < 0 || field >= HP_NFIELDS || n != (size_t)c->I * c->J * c->K) {
+    set_error("hp_read_field: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  if (side == 0) {
+    memcpy(dst, c->host[field], n * sizeof(float));
+    return HP_OK;
+  }
+  CK(cudaMemcpy2DAsync(dst, (size_t)c->K * sizeof(float), c->dev.f[field],
+                       (size_t)c->P * sizeof(float), (size_t)c->K * sizeof(float),
+                       (size_t)c->I * c->J, cudaMemcpyDeviceToHost, c->stream),
+     "read field");
+  CK(cudaStreamSynchronize(c->stream), "read field sync");
+  return HP_OK;
+}
+
+extern "C" int hp_write_field(hp_ctx* c, int field, int side, const float* src, size_t n) {
+  if (!c || !src || field < 0 || field >= HP_NFIELDS || n != (size_t)c->I * c->J * c->K) {
+    set_error("hp_write_field: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  if (side == 0) {
+    memcpy(c->host[field], src, n * sizeof(float));
+    c->host_dirty[field] = true;
+    return HP_OK;
+  }
+  CK(cudaMemcpy2DAsync(c->dev.f[field], (size_t)c->P * sizeof(float), src,
+                       (size_t)c->K * sizeof(float), (size_t)c->K * sizeof(float),
+                       (size_t)c->I * c->J, cudaMemcpyHostToDevice, c->stream),
+     "write field");
+  CK(cudaStreamSynchronize(c->stream), "write field sync");
+  return HP_OK;
+}
+
+extern "C" int hp_read_gosa(hp_ctx* c, int side, double* out) {
+  if (!c || !out) {
+    set_error("hp_read_gosa: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  if (side == 0) {
+    *out = c->hs<double>(HP_V_GOSA);
+    return HP_OK;
+  }
+  CK(cudaMemcpyAsync(out, c->dscal + HP_V_GOSA * SLOT_BYTES, sizeof(double),
+                     cudaMemcpyDeviceToHost, c->stream),
+     "read gosa");
+  CK(cudaStreamSynchronize(c->stream), "read gosa sync");
+  return HP_OK;
+}
+
+// ------------------------------------------------- device-resident Jacobi
+
+static LaunchArgs default_args(const hp_ctx* c, int reset) {
+  LaunchArgs a;
+  a.imax = c->I - 1;
+  a.jmax = c->J - 1;
+  a.kmax = c->K - 1;
+  a.omega = 0.8f;
+  a.gosa_reset = reset;
+  return a;
+}
+
+extern "C" int hp_launches_per_iteration(int variant) { return variant == 1 ? 1 : 2; }
+
+extern "C" int hp_init_device(hp_ctx* c) {
+  if (!c) return HP_ERR_ARG;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const LaunchArgs a = default_args(c, 0);
+  GosaSink g = c->sink();
+  Box b0{0, c->I, 0, c->J, 0, c->K};
+  Box b1{0, a.imax, 0, a.jmax, 0, a.kmax};
+  if (launch_fill(c->dev.f[HP_F_WRK2], c->field_elems, 0.0f, c->stream) < 0 ||
+      launch_nest(NEST_INIT0, MAP_COLLAPSE, c->dev, b0, a, g, c->stream) < 0 ||
+      launch_nest(NEST_INIT1, MAP_COLLAPSE, c->dev, b1, a, g, c->stream) < 0)
+    return cuda_fail(cudaGetLastError(), "init launch");
+  CK(cudaStreamSynchronize(c->stream), "init sync");
+  return HP_OK;
+}
+
+extern "C" int hp_jacobi_device(hp_ctx* c, int nn, int variant) {
+  if (!c || nn < 0 || (variant != 0 && variant != 1)) {
+    set_error("hp_jacobi_device: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const LaunchArgs a = default_args(c, 1);
+  if (variant == 1) {
+    if (nn > 0) {
+      const int n = Runner::time_loop_fused(c, nn, a);
+      if (n < 0) return cuda_fail(cudaGetLastError(), "fused time loop");
+      c->launches += (uint64_t)n;
+    }
+    return HP_OK;
+  }
+  for (int it = 0; it < nn; ++it) {
+    const int r1 = launch_stencil_3d(c->dev, a, c->sink(), c->stream);
+    const int r2 = r1 < 0 ? -1 : launch_copy_3d(c->dev, a, c->stream);
+    if (r1 < 0 || r2 < 0) return cuda_fail(cudaGetLastError(), "time loop");
+    c->launches += (uint64_t)(r1 + r2);
+  }
+  return HP_OK;
+}
+
+extern "C" uint64_t hp_launch_count(hp_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" int hp_time_steps(hp_ctx* c, int steps, int nn, int variant, double* ms_out) {
+  if (!c || !ms_out || steps < 0) {
+    set_error("hp_time_steps: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(cudaEventRecord(c->ev0, c->stream), "event record");
+  for (int s = 0; s < steps; ++s) {
+    const int rc = hp_jacobi_device(c, nn, variant);
+    if (rc != HP_OK) return rc;
+  }
+  CK(cudaEventRecord(c->ev1, c->stream), "event record");
+  CK(cudaEventSynchronize(c->ev1), "event sync");
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event elapsed");
+  *ms_out = ms;
+  return HP_OK;
+}
+
+extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* out) {
+  if (!c || !out || nn < 1 || (variant != 0 && variant != 1)) {
+    set_error("hp_time_jacobi: bad arguments");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  memset(out, 0, sizeof *out);
+  const LaunchArgs a = default_args(c, 1);
+  // one event before every launch and one after the last: launch k spans [k, k+1]
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> is_stencil;
+  auto mark = [&]() -> bool {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return false;
+    ev.push_back(e);
+    return cudaEventRecord(e, c->stream) == cudaSuccess;
+  };
+  bool ok = mark();
+  float* bufs[2] = {c->dev.f[HP_F_P], c->scratch};
+  if (variant == 1) {
+    ok = ok && launch_copy_halo(c->dev, bufs[0], bufs[1], a.imax, a.jmax, a.kmax, c->stream) >= 0;
+    is_stencil.push_back(0);
+    ok = ok && mark();
+    for (int it = 0; ok && it < nn; ++it) {
+      ok = launch_stencil_rotate(c->dev, bufs[it & 1], bufs[(it + 1) & 1], a, c->sink(),
+                                 c->stream) >= 0 && mark();
+      is_stencil.push_back(1);
+    }
+    float* last = bufs[nn & 1];
+    ok = ok && launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a.imax, a.jmax,
+                                           a.kmax, c->stream) >= 0 && mark();
+    is_stencil.push_back(0);
+    if (ok && last != c->dev.f[HP_F_P]) {
+      ok = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a.imax, a.jmax, a.kmax,
+                                       c->stream) >= 0 && mark();
+      is_stencil.push_back(0);
+    }
+  } else {
+    for (int it = 0; ok && it < nn; ++it) {
+      ok = launch_stencil_3d(c->dev, a, c->sink(), c->stream) >= 0 && mark();
+      is_stencil.push_back(1);
+      ok = ok && launch_copy_3d(c->dev, a, c->stream) >= 0 && mark();
+      is_stencil.push_back(0);
+    }
+  }
+  int rc = HP_OK;
+  if (!ok || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    rc = cuda_fail(cudaGetLastError(), "hp_time_jacobi");
+  } else {
+    c->launches += is_stencil.size();
+    double st = 0, ot = 0;
+    for (size_t k = 0; k + 1 < ev.size(); ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      if (is_stencil[k]) { st += ms; out->n_stencil++; }
+      else { ot += ms; out->n_other++; }
+    }
+    float total = 0.f;
+    cudaEventElapsedTime(&total, ev.front(), ev.back());
+    out->total_ms = total;
+    out->stencil_ms = out->n_stencil ? st / out->n_stencil : 0.0;
+    out->other_ms = out->n_other ? ot / out->n_other : 0.0;
+  }
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+extern "C" int hp_jacobi_host(hp_ctx* c, const float* const* fields, int nn, int variant,
+                              float* p_out, double* gosa_out) {
+  if (!c || !fields || !p_out || !gosa_out) {
+    set_error("hp_jacobi_host: null argument");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  for (int f = 0; f < HP_NFIELDS; ++f) {
+    if (f == HP_F_WRK2) continue;
+    if (!fields[f]) {
+      set_error("hp_jacobi_host: field %d missing", f);
+      return HP_ERR_ARG;
+    }
+    CK(cudaMemcpy2DAsync(c->dev.f[f], (size_t)c->P * sizeof(float), fields[f],
+                         (size_t)c->K * sizeof(float), (size_t)c->K * sizeof(float),
+                         (size_t)c->I * c->J, cudaMemcpyHostToDevice, c->stream),
+       "jacobi H2D");
+  }
+  int rc = hp_jacobi_device(c, nn, variant);
+  if (rc != HP_OK) return rc;
+  CK(cudaMemcpy2DAsync(p_out, (size_t)c->K * sizeof(float), c->dev.f[HP_F_P],
+                       (size_t)c->P * sizeof(float), (size_t)c->K * sizeof(float),
+                       (size_t)c->I * c->J, cudaMemcpyDeviceToHost, c->stream),
+     "jacobi D2H p");
+  CK(cudaMemcpyAsync(gosa_out, c->dscal + HP_V_GOSA * SLOT_BYTES, sizeof(double),
+                     cudaMemcpyDeviceToHost, c->stream),
+     "jacobi D2H gosa");
+  CK(cudaStreamSynchronize(c->stream), "jacobi sync");
+  return HP_OK;
+}
+
+extern "C" void* hp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaHostAlloc(%zu) failed", bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+extern "C" void hp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}

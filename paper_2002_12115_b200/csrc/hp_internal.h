@@ -1,0 +1,94 @@
+// Internal declarations shared by kernels.cu and executor.cpp.
+//
+// Device layout: each fp32 field is a
+// pitched [I][J][P] array, P = round_up(K, 32) floats, so every (i, j) row
+// starts on a 128-byte boundary and float4 loads of k-quads are aligned.
+// All 14 fields live in one slab, each at a 2 MiB-aligned offset.
+// Host copies (the program's static arrays) are unpadded [I][J][K] in pinned
+// memory; transfers are 2-D copies (K floats per row).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/himeno_b200.h"
+
+namespace hp {
+
+constexpr int kRowAlign = 32;           // floats per pitch quantum (128 B)
+
+struct DevFields {
+  float* f[HP_NFIELDS];                 // device mirrors
+  int I, J, K, P;                       // extents and row pitch (floats)
+  __host__ __device__ size_t plane() const { return (size_t)J * (size_t)P; }
+  __host__ __device__ size_t at(int i, int j, int k) const {
+    return ((size_t)i * (size_t)J + (size_t)j) * (size_t)P + (size_t)k;
+  }
+};
+
+struct Box {                            // half-open [i0,i1) x [j0,j1) x [k0,k1)
+  int i0, i1, j0, j1, k0, k1;
+  __host__ __device__ long long ni() const { return i1 > i0 ? i1 - i0 : 0; }
+  __host__ __device__ long long nj() const { return j1 > j0 ? j1 - j0 : 0; }
+  __host__ __device__ long long nk() const { return k1 > k0 ? k1 - k0 : 0; }
+  __host__ __device__ long long count() const { return ni() * nj() * nk(); }
+};
+
+// Deterministic gosa reduction target: each block writes a partial, the last
+// block to finish sums the partials in block order and adds (or stores, when
+// `reset`) the total into *slot (the device copy of jacobi's gosa).
+struct GosaSink {
+  double* slot;
+  double* partials;
+  unsigned int* ticket;
+  int capacity;                         // number of partial slots
+};
+
+enum Nest { NEST_INIT0 = 0, NEST_INIT1 = 1, NEST_STENCIL = 2, NEST_COPY = 3 };
+
+// Mapping of a loop-nest execution onto the device (selected by hp_kind).
+enum Mapping {
+  MAP_COLLAPSE = 0,   // kernels: every point of the box is one thread
+  MAP_GANG = 1,       // parallel loop: one CTA per iteration of the box's outer dim
+  MAP_VECTOR = 2      // parallel loop vector: a single CTA strides the box
+};
+
+struct LaunchArgs {
+  int imax, jmax, kmax;                 // program scalars (by value)
+  float omega;
+  int gosa_reset;                       // stencil: store instead of accumulate
+};
+
+// ---- kernels.cu launchers (all enqueue on `s`, no host sync) ----------------
+// Returns number of kernels launched (>=0) or -1 on launch error.
+int launch_nest(Nest nest, Mapping map, const DevFields& F, const Box& box,
+                const LaunchArgs& a, const GosaSink& g, cudaStream_t s);
+// Tuned full-interior stencil (2.5-D blocked, float4) and copy.
+int launch_stencil_3d(const DevFields& F, const LaunchArgs& a, const GosaSink& g,
+                      cudaStream_t s);
+int launch_copy_3d(const DevFields& F, const LaunchArgs& a, cudaStream_t s);
+// Fused time-loop step: reads p_in, writes p_out (interior) -- wrk2 semantics
+// restored at the end of the loop by launch_time_loop_finish.
+int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
+                          const LaunchArgs& a, const GosaSink& g, cudaStream_t s);
+int launch_fill(float* dst, size_t n, float value, cudaStream_t s);
+// dst = src on every point outside the stencil interior
+int launch_copy_halo(const DevFields& F, const float* src, float* dst, int imax, int jmax,
+                     int kmax, cudaStream_t s);
+// dst = src on the interior [1,imax-1) x [1,jmax-1) x [1,kmax-1)
+int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst, int imax,
+                                int jmax, int kmax, cudaStream_t s);
+int gosa_capacity_needed(const DevFields& F);
+
+// ---- host loop bodies (executor.cpp), same arithmetic as the kernels --------
+struct HostFields {
+  float* f[HP_NFIELDS];
+  int I, J, K;
+  size_t at(int i, int j, int k) const {
+    return ((size_t)i * (size_t)J + (size_t)j) * (size_t)K + (size_t)k;
+  }
+};
+
+}  // namespace hp

@@ -1,0 +1,152 @@
+"""GPU parity: the native B200 path against the CPU oracle (run on a B200 box).
+
+Bar: p is bit-exact (every product/sum is rounded
+separately on both sides, no FMA); gosa is an fp64 sum of the same fp32 terms
+in a different order, so |gosa - oracle_fp64| <= 1e-12 * oracle_fp64 -- far
+inside north_star's 1e-5.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2002_12115_b200 import native as N
+from paper_2002_12115_b200.apps import himeno
+from paper_2002_12115_b200.evaluator import B200Evaluator, MeasuredTime, valid_genomes
+from paper_2002_12115_b200.kinds import DirectiveKind
+
+pytestmark = pytest.mark.gpu
+GOSA_RTOL = 1e-12
+
+_ORACLE = {}
+
+
+def oracle_result(name, nn):
+    key = (name, nn)
+    if key not in _ORACLE:
+        sz = himeno.size(name)
+        _ORACLE[key] = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    return _ORACLE[key]
+
+
+def check_run(ev, genome, ref):
+    res = ev.run(genome)
+    assert res.status == 0, res.diag
+    p = ev.read_field("p", side=0)
+    assert np.array_equal(p, ref["fields"]["p"]), f"p differs for {genome}"
+    assert abs(res.gosa - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], (genome, res.gosa)
+    assert res.n_stale_reads == 0, (genome, res.stats())
+    return res
+
+
+@pytest.fixture(scope="module")
+def ev_xs(gpu):
+    ev = B200Evaluator("XS", nn=3, poison_device=True)
+    yield ev
+    ev.close()
+
+
+def test_all_cpu_and_best_patterns(ev_xs):
+    ref = oracle_result("XS", 3)
+    for g in ["0000000000000", "0000000100100", "0000001000000", "1001001000000",
+              "0010010010010", "0100100100100"]:
+        check_run(ev_xs, tuple(int(c) for c in g), ref)
+
+
+def test_every_valid_genome_xs(ev_xs):
+    """All 272 non-nested Himeno genomes reproduce the all-CPU output exactly."""
+    ref = oracle_result("XS", 3)
+    genomes = valid_genomes(ev_xs.loops, ev_xs.eligible_ids)
+    assert len(genomes) == 272
+    for g in genomes:
+        check_run(ev_xs, g, ref)
+
+
+def test_stdout_matches_reference_tokens(ev_xs):
+    out = ev_xs.run_for_output((0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0)).split()
+    want = open("tests/golden/himeno_xs_n3.stdout").read().split()
+    assert out[1:] == want[1:]                      # p samples: exact
+    assert abs(float(out[0]) - float(want[0])) / float(want[0]) < 1e-3  # fp32-seq drift
+
+
+def test_nested_pattern_rejected_before_launch(ev_xs):
+    m = ev_xs.measure((0, 0, 0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0))
+    assert m.failure and "nested" in m.failure
+
+
+def test_per_loop_transfer_mode_moves_more(gpu):
+    ref = oracle_result("XS", 3)
+    g = (0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0)
+    with B200Evaluator("XS", nn=3, transfer_mode="per-loop") as raw, \
+            B200Evaluator("XS", nn=3) as batched:
+        r1 = check_run(raw, g, ref)
+        r2 = check_run(batched, g, ref)
+        assert r1.h2d_bytes + r1.d2h_bytes > 2 * (r2.h2d_bytes + r2.d2h_bytes)
+        assert r1.n_implicit > 0
+
+
+def test_coherence_guard_skips_stale_update(gpu):
+    # 1001001000000: update device(a, b, c, ...) at jacobi entry after device-side init
+    ref = oracle_result("XS", 3)
+    with B200Evaluator("XS", nn=3) as ev:
+        res = check_run(ev, (1, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 0, 0), ref)
+        assert res.n_skipped_stale > 0
+
+
+@pytest.mark.parametrize("kind", [DirectiveKind.PARALLEL_LOOP, DirectiveKind.PARALLEL_LOOP_VECTOR])
+def test_alternative_kinds(gpu, kind):
+    ref = oracle_result("XXS", 3)
+    prog = himeno.program()
+    kinds = {lid: kind for lid in prog.kinds}
+    with B200Evaluator("XXS", nn=3, kinds=kinds) as ev:
+        for g in ["0000000100100", "0100100100100", "0010010010010", "1001001000000",
+                  "0000001000000"]:
+            check_run(ev, tuple(int(c) for c in g), ref)
+
+
+def test_unfused_time_loop(gpu):
+    ref = oracle_result("XS", 3)
+    with B200Evaluator("XS", nn=3, fused_time_loop=False) as ev:
+        check_run(ev, (0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0), ref)
+
+
+def test_timeout_maps_to_measured_timeout(gpu):
+    with B200Evaluator("S", nn=50, timeout_s=0.05) as ev:
+        m = ev.measure((0,) * 13)
+        assert m == MeasuredTime.timeout()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("name,nn", [("XS", 3), ("M", 2)])
+def test_device_jacobi_variants(gpu, variant, name, nn):
+    ref = oracle_result(name, nn)
+    sz = himeno.size(name)
+    with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+        ctx.init_device()
+        ctx.jacobi_device(nn, variant)
+        g = ctx.read_gosa(1)
+        p = ctx.read_field("p", 1)
+        w = ctx.read_field("wrk2", 1)
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert np.array_equal(w, ref["fields"]["wrk2"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+
+
+def test_jacobi_host_e2e(gpu):
+    name, nn = "S", 2
+    sz = himeno.size(name)
+    f = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(f)
+    inputs = {k: v.copy() for k, v in f.items()}
+    g64, _ = oracle.jacobi(f, nn)
+    p_out = np.empty_like(f["p"])
+    with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+        g = ctx.jacobi_host(inputs, nn, 1, p_out)
+    assert np.array_equal(p_out, f["p"])
+    assert abs(g - g64) <= GOSA_RTOL * g64
+
+
+def test_m_grid_selected_patterns(gpu):
+    ref = oracle_result("M", 2)
+    with B200Evaluator("M", nn=2) as ev:
+        for g in ["0000000100100", "1001001000000", "0000001000000", "1001000100100"]:
+            check_run(ev, tuple(int(c) for c in g), ref)

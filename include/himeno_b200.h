@@ -207,6 +207,9 @@ typedef struct hp_kernel_times {
 int hp_time_steps(hp_ctx* ctx, int steps, int nn, int variant, double* ms_out);
 int hp_time_jacobi(hp_ctx* ctx, int nn, int variant, hp_kernel_times* out);
 uint64_t hp_launch_count(hp_ctx* ctx);   /* kernels launched by this context so far */
+/* Tuning sweeps: select the tuned-stencil configuration (vector width x CTAs
+ * per SM, process-wide); returns the number of configurations, <0 if invalid. */
+int hp_set_stencil_config(int cfg);
 
 /* Pinned host buffers for callers without their own allocator (e2e inputs). */
 void* hp_host_alloc(size_t bytes);

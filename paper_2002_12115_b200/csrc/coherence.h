@@ -1,0 +1,88 @@
+#pragma once
+#include <algorithm>
+#include <vector>
+
+#include "hp_internal.h"
+
+namespace hp {
+// Coherence bookkeeping of the device data manager (pure host C++).
+//
+// A chronological log of write boxes, each tagged with the side that holds the
+// latest data there: HOST (host newer), DEV (device newer), BOTH (in sync).
+// Entries fully covered by a later write are pruned, so for Himeno's nested
+// write boxes (full >= [0,max)^3 >= interior) the log never exceeds a few
+// entries.  A guarded transfer copies exactly the region whose latest writer is
+// the source side (a list of disjoint boxes), then marks it in sync.
+enum Owner { OWN_HOST = 0, OWN_DEV = 1, OWN_BOTH = 2 };
+
+inline bool box_empty(const Box& b) { return b.count() <= 0; }
+inline bool box_contains(const Box& o, const Box& in) {
+  if (box_empty(in)) return true;
+  return o.i0 <= in.i0 && in.i1 <= o.i1 && o.j0 <= in.j0 && in.j1 <= o.j1 && o.k0 <= in.k0 &&
+         in.k1 <= o.k1;
+}
+inline Box box_clip(const Box& a, const Box& b) {
+  return Box{std::max(a.i0, b.i0), std::min(a.i1, b.i1), std::max(a.j0, b.j0),
+             std::min(a.j1, b.j1), std::max(a.k0, b.k0), std::min(a.k1, b.k1)};
+}
+inline bool box_meets(const Box& a, const Box& b) { return !box_empty(box_clip(a, b)); }
+inline Box grow(const Box& b, int h) { return Box{b.i0 - h, b.i1 + h, b.j0 - h, b.j1 + h, b.k0 - h, b.k1 + h}; }
+
+// a minus b as up to 6 disjoint boxes
+inline void box_subtract(const Box& a, const Box& b, std::vector<Box>& out) {
+  const Box x = box_clip(a, b);
+  if (box_empty(x)) {
+    if (!box_empty(a)) out.push_back(a);
+    return;
+  }
+  auto put = [&](const Box& q) { if (!box_empty(q)) out.push_back(q); };
+  put(Box{a.i0, x.i0, a.j0, a.j1, a.k0, a.k1});
+  put(Box{x.i1, a.i1, a.j0, a.j1, a.k0, a.k1});
+  put(Box{x.i0, x.i1, a.j0, x.j0, a.k0, a.k1});
+  put(Box{x.i0, x.i1, x.j1, a.j1, a.k0, a.k1});
+  put(Box{x.i0, x.i1, x.j0, x.j1, a.k0, x.k0});
+  put(Box{x.i0, x.i1, x.j0, x.j1, x.k1, a.k1});
+}
+
+struct Coherence {
+  struct Span { Box box; int owner; };
+  std::vector<Span> log;
+
+  void reset(const Box& full) { log.assign(1, Span{full, OWN_HOST}); }
+  void write(const Box& b, int owner) {
+    if (box_empty(b)) return;
+    std::vector<Span> kept;
+    for (const Span& e : log)
+      if (!box_contains(b, e.box)) kept.push_back(e);
+    kept.push_back(Span{b, owner});
+    log.swap(kept);
+  }
+  // disjoint boxes whose latest writer is `owner`
+  std::vector<Box> region(int owner) const {
+    std::vector<Box> out;
+    for (size_t n = 0; n < log.size(); ++n) {
+      if (log[n].owner != owner) continue;
+      std::vector<Box> pieces{log[n].box};
+      for (size_t m = n + 1; m < log.size() && !pieces.empty(); ++m) {
+        std::vector<Box> next;
+        for (const Box& q : pieces) box_subtract(q, log[m].box, next);
+        pieces.swap(next);
+      }
+      out.insert(out.end(), pieces.begin(), pieces.end());
+    }
+    return out;
+  }
+  bool newer_in(int owner, const Box& b) const {
+    for (const Box& q : region(owner))
+      if (box_meets(q, b)) return true;
+    return false;
+  }
+  void mark_synced(int owner) {
+    for (Span& e : log)
+      if (e.owner == owner) e.owner = OWN_BOTH;
+  }
+  void all_synced(const Box& full) { log.assign(1, Span{full, OWN_BOTH}); }
+};
+
+
+}  // namespace hp

@@ -37,6 +37,7 @@
 #include <string>
 #include <vector>
 
+#include "coherence.h"
 #include "hp_internal.h"
 
 using namespace hp;
@@ -142,6 +143,7 @@ struct hp_ctx {
   bool declared[HP_NVARS] = {};
   int refcount[HP_NVARS] = {};
   bool host_dirty[HP_NFIELDS] = {};  // written since the last fresh-process reset
+  Coherence coh[HP_NVARS];           // arrays: which side holds the latest data where
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;         // kernels launched by this context (all entry points)
 
@@ -390,10 +392,51 @@ struct Runner {
     return k == HP_K_KERNELS || k == HP_K_PARALLEL_LOOP || k == HP_K_PLV;
   }
   bool present(int v) const { return C->declared[v] || C->refcount[v] > 0; }
-  void host_write(int v) { C->host_ver[v] = ++C->clock; mark_host_dirty(v); }
-  void dev_write(int v) { C->dev_ver[v] = ++C->clock; }
-  void host_read(int v) { if (C->host_ver[v] < C->dev_ver[v]) R->n_stale_reads++; }
-  void dev_read(int v) { if (C->dev_ver[v] < C->host_ver[v]) R->n_stale_reads++; }
+  Box full_box() const { return Box{0, C->I, 0, C->J, 0, C->K}; }
+  bool is_array(int v) const { return kVars[v].nfields > 0; }
+  void host_write(int v, const Box& b) {
+    if (is_array(v)) C->coh[v].write(b, OWN_HOST);
+    else C->host_ver[v] = ++C->clock;
+    mark_host_dirty(v);
+  }
+  void host_write(int v) { host_write(v, full_box()); }
+  void dev_write(int v, const Box& b) {
+    if (is_array(v)) C->coh[v].write(b, OWN_DEV);
+    else C->dev_ver[v] = ++C->clock;
+  }
+  void host_read(int v, const Box& b) {
+    const bool stale = is_array(v) ? C->coh[v].newer_in(OWN_DEV, b) : C->host_ver[v] < C->dev_ver[v];
+    if (stale) R->n_stale_reads++;
+  }
+  void host_read(int v) { host_read(v, full_box()); }
+  void dev_read(int v, const Box& b) {
+    const bool stale = is_array(v) ? C->coh[v].newer_in(OWN_HOST, b) : C->dev_ver[v] < C->host_ver[v];
+    if (stale) R->n_stale_reads++;
+  }
+  // one field box copy in either direction (2-D fast path for the whole array)
+  bool copy_box(int fid, const Box& b, cudaMemcpyKind kind) {
+    cudaError_t e;
+    const size_t K4 = (size_t)C->K * sizeof(float), P4 = (size_t)C->P * sizeof(float);
+    if (box_contains(b, full_box())) {
+      e = kind == cudaMemcpyHostToDevice
+              ? cudaMemcpy2DAsync(C->dev.f[fid], P4, C->host[fid], K4, K4, (size_t)C->I * C->J,
+                                  kind, C->stream)
+              : cudaMemcpy2DAsync(C->host[fid], K4, C->dev.f[fid], P4, K4, (size_t)C->I * C->J,
+                                  kind, C->stream);
+    } else {
+      cudaMemcpy3DParms m = {};
+      cudaPitchedPtr d = make_cudaPitchedPtr(C->dev.f[fid], P4, K4, (size_t)C->J);
+      cudaPitchedPtr h = make_cudaPitchedPtr(C->host[fid], K4, K4, (size_t)C->J);
+      m.srcPtr = kind == cudaMemcpyHostToDevice ? h : d;
+      m.dstPtr = kind == cudaMemcpyHostToDevice ? d : h;
+      m.srcPos = make_cudaPos((size_t)b.k0 * sizeof(float), (size_t)b.j0, (size_t)b.i0);
+      m.dstPos = m.srcPos;
+      m.extent = make_cudaExtent((size_t)b.nk() * sizeof(float), (size_t)b.nj(), (size_t)b.ni());
+      m.kind = kind;
+      e = cudaMemcpy3DAsync(&m, C->stream);
+    }
+    return cuda_ok(e, kind == cudaMemcpyHostToDevice ? "update device" : "update self");
+  }
   void mark_host_dirty(int v) {
     const VarInfo& vi = kVars[v];
     for (int f = 0; f < vi.nfields; ++f) C->host_dirty[vi.f0 + f] = true;
@@ -408,26 +451,39 @@ struct Runner {
       pending_h2d = false;
     }
   }
+  // Host -> device.  With the guard only the region whose latest data is on
+  // the host is copied (nothing, and counted as skipped, when the host copy
+  // is entirely stale -- SURVEY.md B.2); without it the whole array is copied.
   void h2d(int v, bool implicit) {
     if (failed()) return;
+    const VarInfo& vi = kVars[v];
+    if (vi.nfields) {
+      const std::vector<Box> boxes = guard ? C->coh[v].region(OWN_HOST)
+                                           : std::vector<Box>{full_box()};
+      if (boxes.empty()) {
+        R->n_skipped_stale++;
+        return;
+      }
+      const double t0 = now_s();
+      for (int f = 0; f < vi.nfields; ++f)
+        for (const Box& b : boxes) {
+          if (!copy_box(vi.f0 + f, b, cudaMemcpyHostToDevice)) return;
+          R->h2d_bytes += (uint64_t)b.count() * sizeof(float);
+        }
+      R->n_h2d += (uint64_t)vi.nfields;
+      if (implicit) R->n_implicit++;
+      pending_h2d = true;
+      R->xfer_s += now_s() - t0;
+      if (guard) C->coh[v].mark_synced(OWN_HOST);
+      else C->coh[v].all_synced(full_box());
+      return;
+    }
     if (guard && C->host_ver[v] < C->dev_ver[v]) {
       R->n_skipped_stale++;
       return;
     }
-    const VarInfo& vi = kVars[v];
     const double t0 = now_s();
-    if (vi.nfields) {
-      for (int f = 0; f < vi.nfields; ++f) {
-        const int fid = vi.f0 + f;
-        if (!cuda_ok(cudaMemcpy2DAsync(C->dev.f[fid], (size_t)C->P * sizeof(float), C->host[fid],
-                                       (size_t)C->K * sizeof(float), (size_t)C->K * sizeof(float),
-                                       (size_t)C->I * C->J, cudaMemcpyHostToDevice, C->stream),
-                     "update device"))
-          return;
-        R->h2d_bytes += (uint64_t)C->I * C->J * C->K * sizeof(float);
-        R->n_h2d++;
-      }
-    } else {
+    {
       if (!cuda_ok(cudaMemcpyAsync(C->dscal + v * SLOT_BYTES, C->hscal + v * SLOT_BYTES,
                                    (size_t)vi.bytes, cudaMemcpyHostToDevice, C->stream),
                    "update device (scalar)"))
@@ -440,27 +496,33 @@ struct Runner {
     R->xfer_s += now_s() - t0;
     C->dev_ver[v] = C->host_ver[v];
   }
+  // Device -> host.  With the guard only the region whose latest data is on
+  // the device is copied back, so device memory the program never defined (or
+  // that is older than the host's) never reaches the host; without it the
+  // whole array is copied, as a literal `update self` would.
   void d2h(int v, bool implicit) {
     if (failed()) return;
-    if (guard && C->dev_ver[v] < C->host_ver[v]) {
-      R->n_skipped_stale++;
-      return;
-    }
     const VarInfo& vi = kVars[v];
     const double t0 = now_s();
     if (vi.nfields) {
-      for (int f = 0; f < vi.nfields; ++f) {
-        const int fid = vi.f0 + f;
-        if (!cuda_ok(cudaMemcpy2DAsync(C->host[fid], (size_t)C->K * sizeof(float), C->dev.f[fid],
-                                       (size_t)C->P * sizeof(float), (size_t)C->K * sizeof(float),
-                                       (size_t)C->I * C->J, cudaMemcpyDeviceToHost, C->stream),
-                     "update self"))
-          return;
-        R->d2h_bytes += (uint64_t)C->I * C->J * C->K * sizeof(float);
-        R->n_d2h++;
+      const std::vector<Box> boxes = guard ? C->coh[v].region(OWN_DEV)
+                                           : std::vector<Box>{full_box()};
+      if (boxes.empty()) {
+        R->n_skipped_stale++;
+        return;
       }
+      for (int f = 0; f < vi.nfields; ++f)
+        for (const Box& b : boxes) {
+          if (!copy_box(vi.f0 + f, b, cudaMemcpyDeviceToHost)) return;
+          R->d2h_bytes += (uint64_t)b.count() * sizeof(float);
+        }
+      R->n_d2h += (uint64_t)vi.nfields;
       mark_host_dirty(v);
     } else {
+      if (guard && C->dev_ver[v] < C->host_ver[v]) {
+        R->n_skipped_stale++;
+        return;
+      }
       if (!cuda_ok(cudaMemcpyAsync(C->hscal + v * SLOT_BYTES, C->dscal + v * SLOT_BYTES,
                                    (size_t)vi.bytes, cudaMemcpyDeviceToHost, C->stream),
                    "update self (scalar)"))
@@ -472,7 +534,12 @@ struct Runner {
     cuda_ok(cudaStreamSynchronize(C->stream), "update self (sync)");
     pending_h2d = false;
     R->xfer_s += now_s() - t0;
-    C->host_ver[v] = C->dev_ver[v];
+    if (vi.nfields) {
+      if (guard) C->coh[v].mark_synced(OWN_DEV);
+      else C->coh[v].all_synced(full_box());
+    } else {
+      C->host_ver[v] = C->dev_ver[v];
+    }
   }
 
   // --- plan events ---------------------------------------------------------------
@@ -534,18 +601,19 @@ struct Runner {
     if (nv.gosa && !present(HP_V_GOSA)) out.push_back(HP_V_GOSA);
   }
 
-  void note_device_access(int nest) {
+  // reads/writes of one nest execution over box b (stencil reads p with a halo of 1)
+  void note_device_access(int nest, const Box& b) {
     const NestVars& nv = nest_vars(nest);
     for (int v : nv.arrays) {
-      bool w = std::find(nv.writes.begin(), nv.writes.end(), v) != nv.writes.end();
-      bool r = !(nest == NEST_INIT0 || nest == NEST_INIT1) && !(nest == NEST_STENCIL && v == HP_V_WRK2) &&
-               !(nest == NEST_COPY && v == HP_V_P);
-      if (r) dev_read(v);
-      if (w) dev_write(v);
+      const bool w = std::find(nv.writes.begin(), nv.writes.end(), v) != nv.writes.end();
+      const bool r = !(nest == NEST_INIT0 || nest == NEST_INIT1) &&
+                     !(nest == NEST_STENCIL && v == HP_V_WRK2) && !(nest == NEST_COPY && v == HP_V_P);
+      if (r) dev_read(v, (nest == NEST_STENCIL && v == HP_V_P) ? grow(b, 1) : b);
+      if (w) dev_write(v, b);
     }
     if (nv.gosa) {
-      dev_read(HP_V_GOSA);
-      dev_write(HP_V_GOSA);
+      dev_read(HP_V_GOSA, b);
+      dev_write(HP_V_GOSA, b);
     }
   }
 
@@ -555,7 +623,7 @@ struct Runner {
     implicit_vars(nest, imp);
     for (int v : imp) h2d(v, true);
     if (failed()) return;
-    note_device_access(nest);
+    note_device_access(nest, b);
     const LaunchArgs a = args(0);
     int n;
     if (full_tuned && map == MAP_COLLAPSE && nest == NEST_STENCIL)
@@ -594,7 +662,7 @@ struct Runner {
     if (nest == NEST_STENCIL || nest == NEST_COPY)
       for (int v : nv.arrays)
         if (!(nest == NEST_STENCIL && v == HP_V_WRK2) && !(nest == NEST_COPY && v == HP_V_P))
-          host_read(v);
+          host_read(v, (nest == NEST_STENCIL && v == HP_V_P) ? grow(b, 1) : b);
     switch (nest) {
       case NEST_INIT0: host_init0(H, b); break;
       case NEST_INIT1: host_init1(H, b, C->hs<int>(HP_V_IMAX)); break;
@@ -606,7 +674,7 @@ struct Runner {
       }
       default: host_copy(H, b); break;
     }
-    for (int v : nv.writes) host_write(v);
+    for (int v : nv.writes) host_write(v, b);
     R->host_s += now_s() - t0;
   }
 
@@ -660,7 +728,8 @@ struct Runner {
     const int nn = C->hs<int>(HP_V_NN);
     const int k6 = kind(6);
     const bool fused = (S->flags & HP_FLAG_FUSED_TIME_LOOP) && k6 != HP_K_PLV;
-    for (int v : {HP_V_P, HP_V_BND, HP_V_WRK1, HP_V_A, HP_V_B, HP_V_C}) dev_read(v);
+    const Box interior = nest_box(NEST_STENCIL);
+    if (nn > 0) note_device_access(NEST_STENCIL, interior);
     int n = 0;
     if (nn > 0) {
       if (fused) {
@@ -688,9 +757,9 @@ struct Runner {
     R->n_launch += (uint64_t)n;
     C->launches += (uint64_t)n;
     if (nn > 0) {
-      dev_write(HP_V_WRK2);
-      dev_write(HP_V_P);
-      dev_write(HP_V_GOSA);
+      dev_write(HP_V_WRK2, interior);
+      dev_write(HP_V_P, interior);
+      dev_write(HP_V_GOSA, interior);
     }
     for (int v : imp) d2h(v, true);
   }
@@ -809,6 +878,7 @@ struct Runner {
       C->dev_ver[v] = 0;    // fresh device memory: undefined
       C->declared[v] = false;
       C->refcount[v] = 0;
+      C->coh[v].reset(Box{0, C->I, 0, C->J, 0, C->K});
     }
     memset(C->hscal, 0, HP_NVARS * SLOT_BYTES);
   }
@@ -1007,6 +1077,15 @@ extern "C" int hp_jacobi_device(hp_ctx* c, int nn, int variant) {
 }
 
 extern "C" uint64_t hp_launch_count(hp_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" int hp_set_stencil_config(int cfg) {
+  const int n = set_stencil_config(cfg);
+  if (n < 0) {
+    set_error("hp_set_stencil_config: no configuration %d", cfg);
+    return HP_ERR_ARG;
+  }
+  return n;
+}
 
 extern "C" int hp_time_steps(hp_ctx* c, int steps, int nn, int variant, double* ms_out) {
   if (!c || !ms_out || steps < 0) {

@@ -81,6 +81,8 @@ int launch_copy_halo(const DevFields& F, const float* src, float* dst, int imax,
 int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst, int imax,
                                 int jmax, int kmax, cudaStream_t s);
 int gosa_capacity_needed(const DevFields& F);
+// select the tuned-stencil configuration; returns the number of configs or -1
+int set_stencil_config(int cfg);
 
 // ---- host loop bodies (executor.cpp), same arithmetic as the kernels --------
 struct HostFields {

@@ -232,107 +232,159 @@ __device__ __forceinline__ float4 ldg_stream(const float* ptr) {
   return r;
 }
 
-__device__ __forceinline__ float4 ld4(const float* ptr) {
-  return *reinterpret_cast<const float4*>(ptr);
+// VEC consecutive k values held by one lane (VEC = 2 or 4: 8/16-byte accesses)
+template <int VEC> struct Vec { float e[VEC]; };
+
+template <int VEC> __device__ __forceinline__ Vec<VEC> ldv(const float* p) {
+  Vec<VEC> v;
+  if (VEC == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v.e[0] = t.x; v.e[1] = t.y; v.e[2 % VEC] = t.z; v.e[3 % VEC] = t.w;
+  } else {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    v.e[0] = t.x; v.e[1] = t.y;
+  }
+  return v;
 }
 
-__device__ __forceinline__ float elem(const float4& v, int e) {
-  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+template <int VEC> __device__ __forceinline__ Vec<VEC> ldv_stream(const float* p) {
+  Vec<VEC> v;
+  if (VEC == 4) {
+    const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    v.e[0] = t.x; v.e[1] = t.y; v.e[2 % VEC] = t.z; v.e[3 % VEC] = t.w;
+  } else {
+    const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+    v.e[0] = t.x; v.e[1] = t.y;
+  }
+  return v;
 }
 
-// k-1 neighbour of element 0 and k+1 neighbour of element 3 of a row quad
+template <int VEC> __device__ __forceinline__ void stv(float* p, const float (&r)[VEC]) {
+  if (VEC == 4) *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2 % VEC], r[3 % VEC]);
+  else *reinterpret_cast<float2*>(p) = make_float2(r[0], r[1]);
+}
+
+// k-1 neighbour of element 0 and k+1 neighbour of element VEC-1 of a row vector
 struct Edge { float left, right; };
 
-__device__ __forceinline__ Edge row_edges(const float4& v, const float* row_at_quad, int lane) {
+template <int VEC>
+__device__ __forceinline__ Edge row_edges(const Vec<VEC>& v, const float* row_at, int lane) {
   Edge e;
-  e.left = __shfl_up_sync(0xffffffffu, v.w, 1);
-  e.right = __shfl_down_sync(0xffffffffu, v.x, 1);
-  if (lane == 0) e.left = row_at_quad[-1];
-  if (lane == 31) e.right = row_at_quad[4];
+  e.left = __shfl_up_sync(0xffffffffu, v.e[VEC - 1], 1);
+  e.right = __shfl_down_sync(0xffffffffu, v.e[0], 1);
+  if (lane == 0) e.left = row_at[-1];
+  if (lane == 31) e.right = row_at[VEC];
   return e;
 }
 
-__device__ __forceinline__ float km1(const float4& v, const Edge& e, int x) {
-  return x == 0 ? e.left : elem(v, x - 1);
+template <int VEC>
+__device__ __forceinline__ float km1(const Vec<VEC>& v, const Edge& e, int x) {
+  return x == 0 ? e.left : v.e[x - 1];
 }
-__device__ __forceinline__ float kp1(const float4& v, const Edge& e, int x) {
-  return x == 3 ? e.right : elem(v, x + 1);
+template <int VEC>
+__device__ __forceinline__ float kp1(const Vec<VEC>& v, const Edge& e, int x) {
+  return x == VEC - 1 ? e.right : v.e[x + 1];
+}
+
+// One warp-row column: row j, lane vector starting at kb, planes [ia, ib).
+// Register queue along i holds rows (j-1, j, j+1) of planes i-1 (l*), i (m*),
+// i+1 (n*); k+-1 neighbours come from lane shuffles (+1 scalar load at each
+// warp edge).  Coefficients are streamed (ld.global.cs: read once, evict
+// first) and consumed term by term in the C program's order.
+template <int VEC>
+__device__ __forceinline__ void stencil_column(const DevFields& F, const float* __restrict__ pin,
+                                               float* __restrict__ out, int ia, int ib, int j,
+                                               int kb, int k_lo, int k_hi, float omega, int lane,
+                                               double& acc) {
+  const size_t P = F.P, L = F.plane();
+  const bool active = kb + VEC - 1 >= k_lo && kb < k_hi;  // vector overlaps [k_lo, k_hi)
+  bool ok[VEC];
+  bool full = true;
+#pragma unroll
+  for (int x = 0; x < VEC; ++x) {
+    ok[x] = active && kb + x >= k_lo && kb + x < k_hi;
+    full = full && ok[x];
+  }
+  size_t c = F.at(ia, j, kb);
+  Vec<VEC> l0 = ldv<VEC>(pin + c - L), lm = ldv<VEC>(pin + c - L - P), lp = ldv<VEC>(pin + c - L + P);
+  Vec<VEC> m0 = ldv<VEC>(pin + c), mm = ldv<VEC>(pin + c - P), mp = ldv<VEC>(pin + c + P);
+#pragma unroll 1
+  for (int i = ia; i < ib; ++i, c += L) {
+    const Vec<VEC> n0 = ldv<VEC>(pin + c + L), nm = ldv<VEC>(pin + c + L - P),
+                   np = ldv<VEC>(pin + c + L + P);
+    const Vec<VEC> A0 = ldv_stream<VEC>(F.f[HP_F_A0] + c), A1 = ldv_stream<VEC>(F.f[HP_F_A1] + c);
+    const Vec<VEC> A2 = ldv_stream<VEC>(F.f[HP_F_A2] + c), A3 = ldv_stream<VEC>(F.f[HP_F_A3] + c);
+    const Vec<VEC> B0 = ldv_stream<VEC>(F.f[HP_F_B0] + c), B1 = ldv_stream<VEC>(F.f[HP_F_B1] + c);
+    const Vec<VEC> B2 = ldv_stream<VEC>(F.f[HP_F_B2] + c), C0 = ldv_stream<VEC>(F.f[HP_F_C0] + c);
+    const Vec<VEC> C1 = ldv_stream<VEC>(F.f[HP_F_C1] + c), C2 = ldv_stream<VEC>(F.f[HP_F_C2] + c);
+    const Vec<VEC> W1 = ldv_stream<VEC>(F.f[HP_F_WRK1] + c), BN = ldv_stream<VEC>(F.f[HP_F_BND] + c);
+
+    const Edge eL = row_edges<VEC>(l0, pin + c - L, lane);
+    const Edge eN = row_edges<VEC>(n0, pin + c + L, lane);
+    const Edge eM = row_edges<VEC>(m0, pin + c, lane);
+    const Edge eMm = row_edges<VEC>(mm, pin + c - P, lane);
+    const Edge eMp = row_edges<VEC>(mp, pin + c + P, lane);
+
+    float r[VEC];
+#pragma unroll
+    for (int x = 0; x < VEC; ++x) {
+      float s0 = mul(A0.e[x], n0.e[x]);
+      s0 = add(s0, mul(A1.e[x], mp.e[x]));
+      s0 = add(s0, mul(A2.e[x], kp1<VEC>(m0, eM, x)));
+      s0 = add(s0, mul(B0.e[x], add(sub(sub(np.e[x], nm.e[x]), lp.e[x]), lm.e[x])));
+      s0 = add(s0, mul(B1.e[x], add(sub(sub(kp1<VEC>(mp, eMp, x), kp1<VEC>(mm, eMm, x)),
+                                         km1<VEC>(mp, eMp, x)), km1<VEC>(mm, eMm, x))));
+      s0 = add(s0, mul(B2.e[x], add(sub(sub(kp1<VEC>(n0, eN, x), kp1<VEC>(l0, eL, x)),
+                                         km1<VEC>(n0, eN, x)), km1<VEC>(l0, eL, x))));
+      s0 = add(s0, mul(C0.e[x], l0.e[x]));
+      s0 = add(s0, mul(C1.e[x], mm.e[x]));
+      s0 = add(s0, mul(C2.e[x], km1<VEC>(m0, eM, x)));
+      s0 = add(s0, W1.e[x]);
+      const float ss = mul(sub(mul(s0, A3.e[x]), m0.e[x]), BN.e[x]);
+      r[x] = add(m0.e[x], mul(omega, ss));
+      if (ok[x]) acc += (double)mul(ss, ss);
+    }
+    if (full) {
+      stv<VEC>(out + c, r);
+    } else if (active) {
+#pragma unroll
+      for (int x = 0; x < VEC; ++x)
+        if (ok[x]) out[c + x] = r[x];
+    }
+    lm = mm; l0 = m0; lp = mp;
+    mm = nm; m0 = n0; mp = np;
+  }
 }
 
 // Interior = i in [i_lo, i_hi), j in [j_lo, j_hi), k in [k_lo, k_hi).
-// grid: x = k tiles (128 k), y = j tiles (8 rows), z = i chunks.
-__global__ void __launch_bounds__(kTileWarps * 32, kTargetCtasPerSm)
+// Work unit = (tile, plane), tile = 8 rows x (32*VEC) k, one warp per row.
+// The grid is one wave (SMs x resident CTAs) and CTA b takes the contiguous
+// unit range [U*b/G, U*(b+1)/G) in tile-major, plane-minor order, so every
+// CTA streams the same number of planes (no tail wave).
+template <int VEC, int MINB>
+__global__ void __launch_bounds__(kTileWarps * 32, MINB)
 k_stencil_3d(DevFields F, const float* __restrict__ pin, float* __restrict__ out,
-             int i_lo, int i_hi, int chunk, int j_lo, int j_hi, int k_lo, int k_hi,
+             int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles,
              float omega, GosaSink g, int reset) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int quad = blockIdx.x * kQuadsPerWarp + lane;
-  const int kb = quad * 4;                         // first k of this thread's quad
-  const int j = j_lo + blockIdx.y * kTileWarps + w;
-  const int i0 = i_lo + blockIdx.z * chunk;
-  const int i1 = min(i0 + chunk, i_hi);
-  const size_t P = F.P, L = F.plane();
+  const int ni = i_hi - i_lo;
+  const int jtiles = (j_hi - j_lo + kTileWarps - 1) / kTileWarps;
+  const long long U = (long long)ktiles * jtiles * ni;
+  long long u = U * blockIdx.x / gridDim.x;
+  const long long u_end = U * (blockIdx.x + 1) / gridDim.x;
   double acc = 0.0;
-
-  // whole warp shares j, so this test is warp-uniform and shuffles stay legal
-  if (j < j_hi && i0 < i1) {
-    const bool active = kb + 3 >= k_lo && kb < k_hi;  // quad overlaps [k_lo, k_hi)
-    bool ok[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) ok[x] = active && kb + x >= k_lo && kb + x < k_hi;
-    const bool full = ok[0] && ok[1] && ok[2] && ok[3];
-
-    size_t c = F.at(i0, j, kb);
-    // register queue along i: rows (j-1, j, j+1) of planes i-1 (l*), i (m*), i+1 (n*)
-    float4 l0 = ld4(pin + c - L), lm = ld4(pin + c - L - P), lp = ld4(pin + c - L + P);
-    float4 m0 = ld4(pin + c), mm = ld4(pin + c - P), mp = ld4(pin + c + P);
-    for (int i = i0; i < i1; ++i, c += L) {
-      const float4 n0 = ld4(pin + c + L), nm = ld4(pin + c + L - P), np = ld4(pin + c + L + P);
-      const float4 A0 = ldg_stream(F.f[HP_F_A0] + c), A1 = ldg_stream(F.f[HP_F_A1] + c);
-      const float4 A2 = ldg_stream(F.f[HP_F_A2] + c), A3 = ldg_stream(F.f[HP_F_A3] + c);
-      const float4 B0 = ldg_stream(F.f[HP_F_B0] + c), B1 = ldg_stream(F.f[HP_F_B1] + c);
-      const float4 B2 = ldg_stream(F.f[HP_F_B2] + c), C0 = ldg_stream(F.f[HP_F_C0] + c);
-      const float4 C1 = ldg_stream(F.f[HP_F_C1] + c), C2 = ldg_stream(F.f[HP_F_C2] + c);
-      const float4 W1 = ldg_stream(F.f[HP_F_WRK1] + c), BN = ldg_stream(F.f[HP_F_BND] + c);
-
-      const Edge eL = row_edges(l0, pin + c - L, lane);
-      const Edge eN = row_edges(n0, pin + c + L, lane);
-      const Edge eM = row_edges(m0, pin + c, lane);
-      const Edge eMm = row_edges(mm, pin + c - P, lane);
-      const Edge eMp = row_edges(mp, pin + c + P, lane);
-
-      float r[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        Coef q;
-        q.a0 = elem(A0, x); q.a1 = elem(A1, x); q.a2 = elem(A2, x); q.a3 = elem(A3, x);
-        q.b0 = elem(B0, x); q.b1 = elem(B1, x); q.b2 = elem(B2, x);
-        q.c0 = elem(C0, x); q.c1 = elem(C1, x); q.c2 = elem(C2, x);
-        q.wrk1 = elem(W1, x); q.bnd = elem(BN, x);
-        const float n[19] = {
-            elem(n0, x), elem(mp, x), kp1(m0, eM, x),
-            elem(np, x), elem(nm, x), elem(lp, x), elem(lm, x),
-            kp1(mp, eMp, x), kp1(mm, eMm, x), km1(mp, eMp, x), km1(mm, eMm, x),
-            kp1(n0, eN, x), kp1(l0, eL, x), km1(n0, eN, x), km1(l0, eL, x),
-            elem(l0, x), elem(mm, x), km1(m0, eM, x), elem(m0, x)};
-        const float ss = stencil_ss(q, n);
-        r[x] = add(n[18], mul(omega, ss));
-        if (ok[x]) acc += (double)mul(ss, ss);
-      }
-      if (full) {
-        *reinterpret_cast<float4*>(out + c) = make_float4(r[0], r[1], r[2], r[3]);
-      } else if (active) {
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-          if (ok[x]) out[c + x] = r[x];
-      }
-      lm = mm; l0 = m0; lp = mp;
-      mm = nm; m0 = n0; mp = np;
-    }
+  while (u < u_end) {
+    const int t = (int)(u / ni);
+    const int ia = (int)(u % ni);
+    const int ib = (int)min((long long)ni, (long long)ia + (u_end - u));
+    u += ib - ia;
+    const int kt = t % ktiles, jt = t / ktiles;
+    const int j = j_lo + jt * kTileWarps + w;
+    if (j >= j_hi) continue;  // warp-uniform: shuffles inside stay convergent
+    const int kb = (kt * 32 + lane) * VEC;
+    stencil_column<VEC>(F, pin, out, i_lo + ia, i_lo + ib, j, kb, k_lo, k_hi, omega, lane, acc);
   }
-  const int nblocks = gridDim.x * gridDim.y * gridDim.z;
-  const int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  gosa_commit(g, acc, nblocks, bid, reset);
+  gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
 }
 
 // p[interior] = src[interior] on float4 quads with masked edges.
@@ -439,6 +491,41 @@ static int sm_count() {
   return n;
 }
 
+namespace {
+// Tuned-stencil configurations (vector width, min CTAs/SM); selectable at run
+// time for sweeps (hp_set_stencil_config), default chosen from measurements.
+struct StencilCfg {
+  int vec, minb;
+  void (*fn)(DevFields, const float*, float*, int, int, int, int, int, int, int, float, GosaSink,
+             int);
+};
+const StencilCfg kStencilCfgs[] = {
+    {4, 2, k_stencil_3d<4, 2>}, {4, 1, k_stencil_3d<4, 1>}, {2, 3, k_stencil_3d<2, 3>},
+    {2, 4, k_stencil_3d<2, 4>}, {2, 2, k_stencil_3d<2, 2>}, {4, 3, k_stencil_3d<4, 3>}};
+constexpr int kNumStencilCfgs = sizeof(kStencilCfgs) / sizeof(kStencilCfgs[0]);
+int g_stencil_cfg = 0;
+
+int stencil_grid(int cfg) {
+  static int g[kNumStencilCfgs] = {};
+  if (!g[cfg]) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kStencilCfgs[cfg].fn,
+                                                      kTileWarps * 32, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    g[cfg] = sm_count() * per_sm;
+  }
+  return g[cfg];
+}
+
+}  // namespace
+
+int set_stencil_config(int cfg) {
+  if (cfg < 0 || cfg >= kNumStencilCfgs) return -1;
+  g_stencil_cfg = cfg;
+  return kNumStencilCfgs;
+}
+
 int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
                           const LaunchArgs& a, const GosaSink& g, cudaStream_t s) {
   const int i_lo = 1, i_hi = a.imax - 1, j_lo = 1, j_hi = a.jmax - 1;
@@ -446,21 +533,18 @@ int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) {
     // empty interior: the nest body never runs, gosa keeps (or resets to) 0
     Box b{1, 1, 1, 1, 1, 1};
-    return launch_nest_t<NEST_STENCIL>(MAP_VECTOR, F, b, a, g, s);
+    return launch_nest(NEST_STENCIL, MAP_VECTOR, F, b, a, g, s);
   }
-  const int ktiles = (k_hi + 4 * kQuadsPerWarp - 1) / (4 * kQuadsPerWarp);
+  const StencilCfg& cfg = kStencilCfgs[g_stencil_cfg];
+  const int kspan = 32 * cfg.vec;
+  const int ktiles = (k_hi + kspan - 1) / kspan;
   const int jtiles = (j_hi - j_lo + kTileWarps - 1) / kTileWarps;
-  const int ni = i_hi - i_lo;
-  const int want = sm_count() * kTargetCtasPerSm * 2;
-  int chunks = (want + ktiles * jtiles - 1) / (ktiles * jtiles);
-  if (chunks < 1) chunks = 1;
-  if (chunks > ni) chunks = ni;
-  int chunk = (ni + chunks - 1) / chunks;
-  chunks = (ni + chunk - 1) / chunk;
-  if ((long long)ktiles * jtiles * chunks > g.capacity) return -1;
-  dim3 grid(ktiles, jtiles, chunks);
-  k_stencil_3d<<<grid, kTileWarps * 32, 0, s>>>(F, p_in, p_out, i_lo, i_hi, chunk, j_lo, j_hi,
-                                               k_lo, k_hi, a.omega, g, a.gosa_reset);
+  const long long units = (long long)ktiles * jtiles * (i_hi - i_lo);
+  long long grid = stencil_grid(g_stencil_cfg);
+  if (grid > units) grid = units;
+  if (grid > g.capacity) return -1;
+  cfg.fn<<<(int)grid, kTileWarps * 32, 0, s>>>(F, p_in, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                              ktiles, a.omega, g, a.gosa_reset);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

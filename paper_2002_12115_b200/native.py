@@ -102,6 +102,7 @@ SIGNATURES = {
     "hp_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "hp_time_jacobi": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(KernelTimes)]),
     "hp_launch_count": (C.c_uint64, [_CtxP]),
+    "hp_set_stencil_config": (C.c_int, [C.c_int]),
     "hp_host_alloc": (C.c_void_p, [C.c_size_t]),
     "hp_host_free": (None, [C.c_void_p]),
 }

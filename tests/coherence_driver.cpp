@@ -1,0 +1,63 @@
+// CPU unit driver for csrc/coherence.h (compiled by tests/test_coherence.py).
+#include <cstdio>
+#include <cstdlib>
+
+#include "coherence.h"
+
+using hp::Box;
+using hp::Coherence;
+
+static long long vol(const std::vector<Box>& v) {
+  long long n = 0;
+  for (const Box& b : v) n += b.count();
+  return n;
+}
+#define CHECK(c)                                              \
+  do {                                                        \
+    if (!(c)) {                                               \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); \
+      return 1;                                               \
+    }                                                         \
+  } while (0)
+
+int main() {
+  const Box full{0, 10, 0, 10, 0, 20}, init{0, 9, 0, 9, 0, 19}, in{1, 8, 1, 8, 1, 18};
+  // subtraction: pieces are disjoint and cover a \ b
+  {
+    std::vector<Box> out;
+    hp::box_subtract(full, in, out);
+    CHECK(vol(out) == full.count() - in.count());
+    for (size_t i = 0; i < out.size(); ++i)
+      for (size_t j = i + 1; j < out.size(); ++j) CHECK(!hp::box_meets(out[i], out[j]));
+    out.clear();
+    hp::box_subtract(in, full, out);
+    CHECK(out.empty());
+  }
+  // fresh program: host owns everything, device stale everywhere
+  Coherence c;
+  c.reset(full);
+  CHECK(vol(c.region(hp::OWN_HOST)) == full.count());
+  CHECK(c.region(hp::OWN_DEV).empty());
+  CHECK(c.newer_in(hp::OWN_HOST, in));
+  // 0010000000001: init0 rows on device, init1 on host, copy interior on device
+  c.write(full, hp::OWN_DEV);            // device zeroes everything
+  CHECK(c.log.size() == 1);              // host entry pruned
+  c.mark_synced(hp::OWN_DEV);            // update self after loop 0
+  c.write(init, hp::OWN_HOST);           // host coefficients / p
+  c.write(in, hp::OWN_DEV);              // device copy nest writes the interior
+  const std::vector<Box> dev = c.region(hp::OWN_DEV);
+  CHECK(vol(dev) == in.count());         // only the interior goes back
+  const std::vector<Box> host = c.region(hp::OWN_HOST);
+  CHECK(vol(host) == init.count() - in.count());   // shell init \ interior is host-newer
+  CHECK(c.newer_in(hp::OWN_HOST, hp::grow(in, 1)));  // stencil on device would read stale p
+  CHECK(!c.newer_in(hp::OWN_HOST, Box{3, 4, 3, 4, 3, 4}));
+  c.mark_synced(hp::OWN_DEV);
+  CHECK(c.region(hp::OWN_DEV).empty());
+  // a full host write prunes everything
+  c.write(full, hp::OWN_HOST);
+  CHECK(c.log.size() == 1 && vol(c.region(hp::OWN_HOST)) == full.count());
+  c.all_synced(full);
+  CHECK(c.region(hp::OWN_HOST).empty() && c.region(hp::OWN_DEV).empty());
+  std::printf("OK\n");
+  return 0;
+}

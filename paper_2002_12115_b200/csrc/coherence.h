@@ -11,8 +11,10 @@ namespace hp {
 // latest data there: HOST (host newer), DEV (device newer), BOTH (in sync).
 // Entries fully covered by a later write are pruned, so for Himeno's nested
 // write boxes (full >= [0,max)^3 >= interior) the log never exceeds a few
-// entries.  A guarded transfer copies exactly the region whose latest writer is
-// the source side (a list of disjoint boxes), then marks it in sync.
+// entries.  A guarded transfer copies everything except the region where the
+// destination holds newer data (a list of disjoint boxes), then marks the
+// source's newer region in sync.  Device memory that was never defined (or was
+// deallocated at a data-region exit) is modelled as HOST-owned.
 enum Owner { OWN_HOST = 0, OWN_DEV = 1, OWN_BOTH = 2 };
 
 inline bool box_empty(const Box& b) { return b.count() <= 0; }
@@ -76,6 +78,17 @@ struct Coherence {
     for (const Box& q : region(owner))
       if (box_meets(q, b)) return true;
     return false;
+  }
+  // points whose latest writer is NOT `owner` (the region a guarded transfer
+  // from the other side may copy without clobbering newer data)
+  std::vector<Box> region_excluding(int owner, const Box& full) const {
+    std::vector<Box> keep{full};
+    for (const Box& q : region(owner)) {
+      std::vector<Box> next;
+      for (const Box& k : keep) box_subtract(k, q, next);
+      keep.swap(next);
+    }
+    return keep;
   }
   void mark_synced(int owner) {
     for (Span& e : log)

@@ -181,6 +181,7 @@ extern "C" void hp_destroy(hp_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->dev.tma) destroy_stencil_tma(const_cast<void*>(c->dev.tma));
   if (c->slab) cudaFree(c->slab);
   if (c->dscal) cudaFree(c->dscal);
   if (c->partials) cudaFree(c->partials);
@@ -256,6 +257,7 @@ extern "C" int hp_create(int device, const hp_grid* grid, int flags, hp_ctx** ou
   cudaMemsetAsync(c->slab, 0, slab_elems * sizeof(float), c->stream);
   cudaEventCreate(&c->ev0);
   cudaEventCreate(&c->ev1);
+  c->dev.tma = create_stencil_tma(c->dev, c->scratch);   // nullptr: register kernel only
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess)
     return fail(cuda_fail(e, "context init"));
   (void)rc;
@@ -451,14 +453,14 @@ struct Runner {
       pending_h2d = false;
     }
   }
-  // Host -> device.  With the guard only the region whose latest data is on
-  // the host is copied (nothing, and counted as skipped, when the host copy
-  // is entirely stale -- SURVEY.md B.2); without it the whole array is copied.
+  // Host -> device.  With the guard every point is copied except those whose
+  // latest data is on the device (nothing, counted as skipped, when the host
+  // copy is entirely stale -- SURVEY.md B.2); without it the whole array is.
   void h2d(int v, bool implicit) {
     if (failed()) return;
     const VarInfo& vi = kVars[v];
     if (vi.nfields) {
-      const std::vector<Box> boxes = guard ? C->coh[v].region(OWN_HOST)
+      const std::vector<Box> boxes = guard ? C->coh[v].region_excluding(OWN_DEV, full_box())
                                            : std::vector<Box>{full_box()};
       if (boxes.empty()) {
         R->n_skipped_stale++;
@@ -496,16 +498,16 @@ struct Runner {
     R->xfer_s += now_s() - t0;
     C->dev_ver[v] = C->host_ver[v];
   }
-  // Device -> host.  With the guard only the region whose latest data is on
-  // the device is copied back, so device memory the program never defined (or
-  // that is older than the host's) never reaches the host; without it the
-  // whole array is copied, as a literal `update self` would.
+  // Device -> host.  With the guard every point is copied back except those
+  // whose latest data is on the host -- which includes device memory the
+  // program never defined -- so undefined or older device data never reaches
+  // the host; without it the whole array is copied, as a literal `update self`.
   void d2h(int v, bool implicit) {
     if (failed()) return;
     const VarInfo& vi = kVars[v];
     const double t0 = now_s();
     if (vi.nfields) {
-      const std::vector<Box> boxes = guard ? C->coh[v].region(OWN_DEV)
+      const std::vector<Box> boxes = guard ? C->coh[v].region_excluding(OWN_HOST, full_box())
                                            : std::vector<Box>{full_box()};
       if (boxes.empty()) {
         R->n_skipped_stale++;
@@ -542,6 +544,13 @@ struct Runner {
     }
   }
 
+  // A structured data region (or an implicit per-kernel copy) ends: the device
+  // copy is deallocated, its contents undefined from now on.
+  void dealloc(int v) {
+    if (is_array(v)) C->coh[v].reset(full_box());
+    else C->dev_ver[v] = 0;
+  }
+
   // --- plan events ---------------------------------------------------------------
   void fire(const hp_event* e) {
     if (failed()) return;
@@ -566,7 +575,10 @@ struct Runner {
         break;
       case HP_EV_DATA_EXIT:
         if (C->declared[v]) break;
-        if (C->refcount[v] > 0 && --C->refcount[v] == 0 && e->arg) d2h(v, false);
+        if (C->refcount[v] > 0 && --C->refcount[v] == 0) {
+          if (e->arg) d2h(v, false);
+          dealloc(v);
+        }
         break;
       case HP_EV_PRESENT:
         if (!present(v))
@@ -639,7 +651,10 @@ struct Runner {
     }
     R->n_launch += (uint64_t)n;
     C->launches += (uint64_t)n;
-    for (int v : imp) d2h(v, true);
+    for (int v : imp) {
+      d2h(v, true);
+      dealloc(v);
+    }
   }
 
   // --- nests ---------------------------------------------------------------------
@@ -761,7 +776,10 @@ struct Runner {
       dev_write(HP_V_P, interior);
       dev_write(HP_V_GOSA, interior);
     }
-    for (int v : imp) d2h(v, true);
+    for (int v : imp) {
+      d2h(v, true);
+      dealloc(v);
+    }
   }
 
  public:

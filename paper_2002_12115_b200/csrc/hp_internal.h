@@ -22,6 +22,7 @@ constexpr int kRowAlign = 32;           // floats per pitch quantum (128 B)
 struct DevFields {
   float* f[HP_NFIELDS];                 // device mirrors
   int I, J, K, P;                       // extents and row pitch (floats)
+  const void* tma;                      // host handle: TMA tensor maps (stencil_tma.cu)
   __host__ __device__ size_t plane() const { return (size_t)J * (size_t)P; }
   __host__ __device__ size_t at(int i, int j, int k) const {
     return ((size_t)i * (size_t)J + (size_t)j) * (size_t)P + (size_t)k;
@@ -83,6 +84,12 @@ int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst
 int gosa_capacity_needed(const DevFields& F);
 // select the tuned-stencil configuration; returns the number of configs or -1
 int set_stencil_config(int cfg);
+// stencil_tma.cu: tensor maps of one context and the TMA-pipelined stencil
+void* create_stencil_tma(const DevFields& F, const float* scratch);
+void destroy_stencil_tma(void* h);
+int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                       const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int stages,
+                       int sms);
 
 // ---- host loop bodies (executor.cpp), same arithmetic as the kernels --------
 struct HostFields {

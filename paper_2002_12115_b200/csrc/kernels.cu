@@ -24,6 +24,7 @@
 #include <cstdio>
 
 #include "hp_internal.h"
+#include "reduce.cuh"
 
 namespace hp {
 namespace {
@@ -101,55 +102,6 @@ __device__ __forceinline__ float body_stencil(const DevFields& F, const float* _
   acc += (double)mul(ss, ss);
   out[c] = add(n[18], mul(omega, ss));
   return ss;
-}
-
-// ------------------------------------------------------------- reductions
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block sum in fixed order; result valid in thread 0.
-__device__ double block_sum(double v) {
-  __shared__ double warp_part[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) warp_part[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (w == 0) {
-    t = lane < nw ? warp_part[lane] : 0.0;
-    t = warp_sum(t);
-  }
-  return t;
-}
-
-// Every block calls this exactly once with its partial; the last block to
-// arrive folds all partials (in block order) into *slot.
-__device__ void gosa_commit(const GosaSink& g, double v, int nblocks, int block_id, int reset) {
-  __shared__ bool last;
-  const double s = block_sum(v);
-  if (threadIdx.x == 0) {
-    g.partials[block_id] = s;
-    __threadfence();
-    const unsigned t = atomicAdd(g.ticket, 1u);
-    last = (t == (unsigned)nblocks - 1u);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double acc = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
-    acc += ((volatile double*)g.partials)[b];
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) {
-    *g.slot = reset ? acc : (*g.slot + acc);
-    *g.ticket = 0u;
-  }
 }
 
 // -------------------------------------------------------- generic nest kernel
@@ -498,15 +450,18 @@ struct StencilCfg {
   int vec, minb;
   void (*fn)(DevFields, const float*, float*, int, int, int, int, int, int, int, float, GosaSink,
              int);
+  int tma_stages;   // > 0: TMA-pipelined kernel (stencil_tma.cu) with this many stages
 };
 const StencilCfg kStencilCfgs[] = {
-    {4, 2, k_stencil_3d<4, 2>}, {4, 1, k_stencil_3d<4, 1>}, {2, 3, k_stencil_3d<2, 3>},
-    {2, 4, k_stencil_3d<2, 4>}, {2, 2, k_stencil_3d<2, 2>}, {4, 3, k_stencil_3d<4, 3>}};
+    {4, 2, k_stencil_3d<4, 2>, 0}, {4, 1, k_stencil_3d<4, 1>, 0}, {2, 3, k_stencil_3d<2, 3>, 0},
+    {2, 4, k_stencil_3d<2, 4>, 0}, {2, 2, k_stencil_3d<2, 2>, 0}, {4, 3, k_stencil_3d<4, 3>, 0},
+    {4, 1, nullptr, 2},            {4, 1, nullptr, 3},            {4, 1, nullptr, 4}};
 constexpr int kNumStencilCfgs = sizeof(kStencilCfgs) / sizeof(kStencilCfgs[0]);
 int g_stencil_cfg = 0;
 
 int stencil_grid(int cfg) {
   static int g[kNumStencilCfgs] = {};
+  if (!kStencilCfgs[cfg].fn) return sm_count();
   if (!g[cfg]) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kStencilCfgs[cfg].fn,
@@ -535,12 +490,17 @@ int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
     Box b{1, 1, 1, 1, 1, 1};
     return launch_nest(NEST_STENCIL, MAP_VECTOR, F, b, a, g, s);
   }
-  const StencilCfg& cfg = kStencilCfgs[g_stencil_cfg];
+  if (kStencilCfgs[g_stencil_cfg].tma_stages > 0) {
+    const int r = launch_stencil_tma(F, F.tma, p_in, p_out, a, g, s,
+                                     kStencilCfgs[g_stencil_cfg].tma_stages, sm_count());
+    if (r != 0) return r;           // else: no tensor maps -> register kernel below
+  }
+  const StencilCfg& cfg = kStencilCfgs[kStencilCfgs[g_stencil_cfg].fn ? g_stencil_cfg : 0];
   const int kspan = 32 * cfg.vec;
   const int ktiles = (k_hi + kspan - 1) / kspan;
   const int jtiles = (j_hi - j_lo + kTileWarps - 1) / kTileWarps;
   const long long units = (long long)ktiles * jtiles * (i_hi - i_lo);
-  long long grid = stencil_grid(g_stencil_cfg);
+  long long grid = stencil_grid(kStencilCfgs[g_stencil_cfg].fn ? g_stencil_cfg : 0);
   if (grid > units) grid = units;
   if (grid > g.capacity) return -1;
   cfg.fn<<<(int)grid, kTileWarps * 32, 0, s>>>(F, p_in, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,

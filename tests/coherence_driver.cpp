@@ -46,13 +46,19 @@ int main() {
   c.write(init, hp::OWN_HOST);           // host coefficients / p
   c.write(in, hp::OWN_DEV);              // device copy nest writes the interior
   const std::vector<Box> dev = c.region(hp::OWN_DEV);
-  CHECK(vol(dev) == in.count());         // only the interior goes back
+  CHECK(vol(dev) == in.count());         // only the interior is device-newer
+  // a guarded update self copies everything but the host-newer shell init \ interior
+  CHECK(vol(c.region_excluding(hp::OWN_HOST, full)) == full.count() - (init.count() - in.count()));
   const std::vector<Box> host = c.region(hp::OWN_HOST);
   CHECK(vol(host) == init.count() - in.count());   // shell init \ interior is host-newer
   CHECK(c.newer_in(hp::OWN_HOST, hp::grow(in, 1)));  // stencil on device would read stale p
   CHECK(!c.newer_in(hp::OWN_HOST, Box{3, 4, 3, 4, 3, 4}));
   c.mark_synced(hp::OWN_DEV);
   CHECK(c.region(hp::OWN_DEV).empty());
+  // after a deallocation the device is undefined: an update device copies everything
+  c.reset(full);
+  CHECK(vol(c.region_excluding(hp::OWN_DEV, full)) == full.count());
+  CHECK(c.region_excluding(hp::OWN_HOST, full).empty());   // nothing defined to copy back
   // a full host write prunes everything
   c.write(full, hp::OWN_HOST);
   CHECK(c.log.size() == 1 && vol(c.region(hp::OWN_HOST)) == full.count());

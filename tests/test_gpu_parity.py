@@ -80,7 +80,7 @@ def test_per_loop_transfer_mode_moves_more(gpu):
             B200Evaluator("XS", nn=3) as batched:
         r1 = check_run(raw, g, ref)
         r2 = check_run(batched, g, ref)
-        assert r1.h2d_bytes + r1.d2h_bytes > 2 * (r2.h2d_bytes + r2.d2h_bytes)
+        assert r1.h2d_bytes + r1.d2h_bytes > 2 * (r2.h2d_bytes + r2.d2h_bytes), (r1.stats(), r2.stats())
         assert r1.n_implicit > 0
 
 
@@ -150,3 +150,25 @@ def test_m_grid_selected_patterns(gpu):
     with B200Evaluator("M", nn=2) as ev:
         for g in ["0000000100100", "1001001000000", "0000001000000", "1001000100100"]:
             check_run(ev, tuple(int(c) for c in g), ref)
+
+
+@pytest.mark.parametrize("name,nn", [("XS", 2), ("M", 2), ("custom", 3)])
+def test_every_stencil_config_bit_exact(gpu, name, nn):
+    """Register and TMA stencil variants all reproduce the oracle exactly."""
+    sz = himeno.custom_size(37, 21, 70) if name == "custom" else himeno.size(name)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    lib = N.load()
+    ncfg = lib.hp_set_stencil_config(0)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            for cfg in range(ncfg):
+                assert lib.hp_set_stencil_config(cfg) == ncfg
+                for variant in (0, 1):
+                    ctx.init_device()
+                    ctx.jacobi_device(nn, variant)
+                    p = ctx.read_field("p", 1)
+                    g = ctx.read_gosa(1)
+                    assert np.array_equal(p, ref["fields"]["p"]), (cfg, variant)
+                    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], (cfg, variant)
+    finally:
+        lib.hp_set_stencil_config(0)

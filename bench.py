@@ -247,7 +247,7 @@ def run_ours(args, world, rank, local):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_stencil_3d (fused time loop)" if variant == 1 else "k_stencil_3d",
+                "kernel": "k_stencil_tma<3> (TMA ring; fused time loop)" if variant == 1 else "k_stencil_tma<3>",
                 "bytes_per_point": BYTES_STENCIL, "points_per_launch": size.interior_points,
                 "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,
                 "peak_source": peak_src}

@@ -457,7 +457,7 @@ const StencilCfg kStencilCfgs[] = {
     {2, 4, k_stencil_3d<2, 4>, 0}, {2, 2, k_stencil_3d<2, 2>, 0}, {4, 3, k_stencil_3d<4, 3>, 0},
     {4, 1, nullptr, 2},            {4, 1, nullptr, 3},            {4, 1, nullptr, 4}};
 constexpr int kNumStencilCfgs = sizeof(kStencilCfgs) / sizeof(kStencilCfgs[0]);
-int g_stencil_cfg = 0;
+int g_stencil_cfg = 7;   // TMA, 3 stages: best on M/L/XL (profiles/)
 
 int stencil_grid(int cfg) {
   static int g[kNumStencilCfgs] = {};

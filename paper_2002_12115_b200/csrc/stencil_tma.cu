@@ -363,11 +363,13 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   if (grid > units) grid = units;
   if (grid > g.capacity) return -1;
   const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t);
+  static bool attr_set[5] = {};   // per stage count: raise the dynamic smem limit once
   auto launch = [&](auto kern) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+    if (!attr_set[stages]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return;
+      attr_set[stages] = true;
     }
     kern<<<(int)grid, kThreads, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
                                            ktiles, a.omega, g, a.gosa_reset);

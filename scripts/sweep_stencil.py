@@ -46,7 +46,7 @@ def main():
             print(json.dumps({"cfg": cfg, "size": sz.name, "stencil_ms": best.stencil_ms,
                               "gbs": gbs, "other_ms": best.other_ms, "total_ms": best.total_ms,
                               "gosa": gosa, "p_same_as_cfg0": same}), flush=True)
-        lib.hp_set_stencil_config(0)
+        lib.hp_set_stencil_config(7)
 
 
 if __name__ == "__main__":

@@ -19,9 +19,9 @@ so no flush is needed between steps.  GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
 * ga         run_ga (pop 20 x gen 10, Himeno M, nn=3) with B200Evaluator on this
              rank's GPU: fresh evaluations/s and generations/s.
 
-N > 1 (torchrun): each rank runs the full workload on its own GPU (replicas;
-DESIGN.md §Multi-GPU -- the slab decomposition is not wired into bench yet);
-scaling "weak".  --impl reference: rank 0 times the CPU reference path
+N > 1 (torchrun): the grid is split into N slabs of i-planes (dd.SlabJacobi), one
+per GPU; halo planes and the gosa all-reduce go over NCCL; "scaling": "strong"
+(total work fixed).  --impl reference: rank 0 times the CPU reference path
 (oracle jacobi, OpenMP over all host cores); other ranks exit 0.
 """
 
@@ -208,17 +208,26 @@ def run_ours(args, world, rank, local):
 
     size = himeno.size(args.size)
     nn, variant = args.nn, args.variant
-    flops_step = FLOP_PER_POINT * size.interior_points * nn
-    ctx = N.Context(local, size.I, size.J, size.K)
-    ctx.init_device()
+    flops_step = FLOP_PER_POINT * size.interior_points * nn      # whole grid, one step
+    slab = None
+    if world > 1:
+        # strong scaling: the grid is split into slabs, halo planes + gosa over NCCL
+        from paper_2002_12115_b200.dd import SlabJacobi
+        slab = SlabJacobi(size, rank, world, local, dist=dist)
+        ctx = slab.ctx
+        timed = lambda k: slab.time_steps(k, nn)           # noqa: E731
+    else:
+        ctx = N.Context(local, size.I, size.J, size.K)
+        ctx.init_device()
+        timed = lambda k: ctx.time_steps(k, nn, variant)   # noqa: E731
     for _ in range(args.warmup):
-        ctx.time_steps(1, nn, variant)
+        timed(1)
 
     n0 = ctx.launch_count
     with ClockSampler(local) as clocks:
         barrier()
         torch.cuda.synchronize()
-        ms = ctx.time_steps(args.steps, nn, variant)
+        ms = timed(args.steps)
         torch.cuda.synchronize()
         barrier()
     launches = ctx.launch_count - n0
@@ -228,16 +237,17 @@ def run_ours(args, world, rank, local):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-    value = world * args.steps * flops_step / (ms_max / 1e3) / 1e9
+    value = args.steps * flops_step / (ms_max / 1e3) / 1e9
 
     # correctness of the timed state: gosa finite and positive
     gosa = ctx.read_gosa(1)
     assert gosa == gosa and gosa > 0, f"bad gosa {gosa}"
 
     # dominant kernel (the stencil launch), CUDA events per launch
-    kt = ctx.time_jacobi(nn, variant)
+    kt = ctx.time_jacobi(nn, variant)      # this rank's grid or slab, no exchange
     peak, peak_src = peaks()
-    achieved = BYTES_STENCIL * size.interior_points / (kt.stencil_ms / 1e3) / 1e9
+    points = slab.interior_points if slab is not None else size.interior_points
+    achieved = BYTES_STENCIL * points / (kt.stencil_ms / 1e3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
@@ -248,39 +258,58 @@ def run_ours(args, world, rank, local):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "k_stencil_tma<3> (TMA ring; fused time loop)" if variant == 1 else "k_stencil_tma<3>",
-                "bytes_per_point": BYTES_STENCIL, "points_per_launch": size.interior_points,
+                "bytes_per_point": BYTES_STENCIL, "points_per_launch": points,
                 "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,
                 "peak_source": peak_src}
 
-    # e2e through the C ABI with pinned host buffers
+    # e2e through the C ABI with pinned host buffers: H2D of the inputs, the
+    # time loop, D2H of p and gosa, every step (per rank: its slab)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    import ctypes
     host = {}
     ctx.init_device()
-    import ctypes
     pinned = []
-    nbytes = size.I * size.J * size.K * 4
+    I_loc = ctx.shape[0]
+    nbytes = I_loc * size.J * size.K * 4
     for name in N.FIELDS:
         ptr = ctx.lib.hp_host_alloc(nbytes)
         if not ptr:
             raise RuntimeError("pinned allocation failed")
         pinned.append(ptr)
         arr = np.ctypeslib.as_array((ctypes.c_float * (nbytes // 4)).from_address(ptr))
-        host[name] = arr.reshape(size.I, size.J, size.K)
+        host[name] = arr.reshape(I_loc, size.J, size.K)
         host[name][...] = ctx.read_field(name, 1)
     p_out = host["wrk2"]   # wrk2 is not an input; reuse its pinned buffer for p
-    ctx.jacobi_host(host, nn, variant, p_out)     # warm-up
+
+    def e2e_step():
+        if slab is None:
+            return ctx.jacobi_host(host, nn, variant, p_out)
+        for name in N.FIELDS:
+            if name != "wrk2":
+                ctx.write_field(name, 1, host[name])
+        slab.jacobi(nn)
+        p_out[...] = ctx.read_field("p", 1)
+        return ctx.read_gosa(1)
+
+    e2e_step()     # warm-up
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        ctx.jacobi_host(host, nn, variant, p_out)
+        e2e_step()
     e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
     barrier()
     for ptr in pinned:
         ctx.lib.hp_host_free(ptr)
-    e2e_value = world * e2e_steps * flops_step / e2e_s / 1e9
+    e2e_value = e2e_steps * flops_step / e2e_s / 1e9
     e2e = {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": 13 * nbytes,
            "d2h_bytes_per_step": nbytes + 8, "steps": e2e_steps,
-           "ms_per_step": e2e_s * 1e3 / e2e_steps, "path": "hp_jacobi_host (C ABI), pinned host"}
+           "ms_per_step": e2e_s * 1e3 / e2e_steps,
+           "path": "hp_jacobi_host (C ABI), pinned host" if slab is None
+                   else "hp_write_field + hp_dd_jacobi + hp_read_field per slab (C ABI)"}
 
     extra = {}
     if rank == 0 and not args.no_cpu_baseline:
@@ -289,18 +318,23 @@ def run_ours(args, world, rank, local):
     if rank == 0 and not args.no_ga:
         extra["ga"] = ga_throughput(local, args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
                                     args.ga_seed)
-    ctx.close()
+    if slab is not None:
+        slab.close()
+    else:
+        ctx.close()
 
     if rank == 0:
         line = {
             "metric": "Himeno GFLOPS", "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Himeno initmt state, deterministic)",
             "config": {"workload": f"himeno_{size.name}_jacobi", "grid": [size.I, size.J, size.K],
                        "nn_per_step": nn, "pattern": "0000001000000 (device time loop)",
                        "variant": "fused rotation" if variant == 1 else "stencil+copy",
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"slab{world} (i-planes, NCCL halo + gosa all-reduce)"
+                       if world > 1 else "single",
                        "l2": "inputs 1.9 GB > 126 MB L2 (no flush)"},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "gosa": gosa,

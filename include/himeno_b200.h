@@ -211,6 +211,25 @@ uint64_t hp_launch_count(hp_ctx* ctx);   /* kernels launched by this context so 
  * per SM, process-wide); returns the number of configurations, <0 if invalid. */
 int hp_set_stencil_config(int cfg);
 
+/* ---- slab decomposition over several GPUs -----------------
+ * The interior planes [1, I-2) of the slowest dimension are split into
+ * contiguous slabs (hp_slab_range); a slab context holds global planes
+ * [i_begin-1, i_end+1) (its interior + one halo plane each side) and supports
+ * hp_init_device / hp_read_field (local planes) / hp_read_gosa.
+ * hp_group_jacobi: one thread drives n slab contexts (in-process; halo planes by
+ * cudaMemcpyPeerAsync, also usable with several slabs on one GPU); *gosa_out =
+ * global gosa.  hp_dd_*: one process per GPU over NCCL (dlopen'ed libnccl.so.2):
+ * rank 0 makes the id with hp_nccl_unique_id, every rank passes it to
+ * hp_dd_init; hp_dd_jacobi enqueues nn iterations with halo send/recv after each
+ * and one fp64 all-reduce of gosa (read it with hp_read_gosa(ctx, 1, ...)). */
+int hp_slab_range(int I, int nranks, int rank, int32_t* i_begin, int32_t* i_end);
+int hp_create_slab(int device, const hp_grid* global, int i_begin, int i_end, hp_ctx** out);
+int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out);
+int hp_nccl_unique_id(unsigned char* out, size_t n);
+int hp_dd_init(hp_ctx* ctx, int nranks, int rank, const unsigned char* id, size_t n);
+int hp_dd_jacobi(hp_ctx* ctx, int nn);
+int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
+
 /* Pinned host buffers for callers without their own allocator (e2e inputs). */
 void* hp_host_alloc(size_t bytes);
 void hp_host_free(void* p);

@@ -84,7 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
-          "-Xlinker", "-soname=libhimeno_b200.so"], verbose)
+          "-Xlinker", "-soname=libhimeno_b200.so", "-ldl"], verbose)
     os.replace(tmp, LIB)
     for obj in objs:
         obj.unlink(missing_ok=True)

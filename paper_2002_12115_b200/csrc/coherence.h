@@ -46,17 +46,42 @@ inline void box_subtract(const Box& a, const Box& b, std::vector<Box>& out) {
   put(Box{x.i0, x.i1, x.j0, x.j1, x.k1, a.k1});
 }
 
+// a and b form exactly one box together (one contains the other, or they agree
+// on two dimensions and overlap / touch on the third)
+inline bool box_union_is_box(const Box& a, const Box& b) {
+  if (box_contains(a, b) || box_contains(b, a)) return true;
+  const bool si = a.i0 == b.i0 && a.i1 == b.i1, sj = a.j0 == b.j0 && a.j1 == b.j1,
+             sk = a.k0 == b.k0 && a.k1 == b.k1;
+  if (si && sj) return a.k1 >= b.k0 && b.k1 >= a.k0;
+  if (si && sk) return a.j1 >= b.j0 && b.j1 >= a.j0;
+  if (sj && sk) return a.i1 >= b.i0 && b.i1 >= a.i0;
+  return false;
+}
+inline Box box_hull(const Box& a, const Box& b) {
+  return Box{std::min(a.i0, b.i0), std::max(a.i1, b.i1), std::min(a.j0, b.j0),
+             std::max(a.j1, b.j1), std::min(a.k0, b.k0), std::max(a.k1, b.k1)};
+}
+
 struct Coherence {
   struct Span { Box box; int owner; };
   std::vector<Span> log;
 
   void reset(const Box& full) { log.assign(1, Span{full, OWN_HOST}); }
+  // Record a write.  Consecutive writes of the same side coalesce while their
+  // union is a box (row launches -> planes -> slabs), and entries the write
+  // covers are dropped, so the log stays a handful of boxes.
   void write(const Box& b, int owner) {
     if (box_empty(b)) return;
+    Box nb = b;
+    while (!log.empty() && log.back().owner == owner && box_union_is_box(log.back().box, nb)) {
+      nb = box_hull(log.back().box, nb);
+      log.pop_back();
+    }
     std::vector<Span> kept;
+    kept.reserve(log.size() + 1);
     for (const Span& e : log)
-      if (!box_contains(b, e.box)) kept.push_back(e);
-    kept.push_back(Span{b, owner});
+      if (!box_contains(nb, e.box)) kept.push_back(e);
+    kept.push_back(Span{nb, owner});
     log.swap(kept);
   }
   // disjoint boxes whose latest writer is `owner`

@@ -1,0 +1,333 @@
+// Slab decomposition of the device-resident Jacobi over several GPUs.
+//
+// The interior planes [1, I-2) of the slowest dimension (C `i`) are split into
+// contiguous slabs, one per rank.  A slab context holds global planes
+// [i_begin-1, i_end+1): its interior plus one halo plane on each side (a global
+// boundary plane at the ends of the grid).  Per iteration each rank runs the
+// fused stencil on its interior, then exchanges the planes its neighbours
+// need -- its first interior plane goes to rank-1's upper halo, its last to
+// rank+1's lower halo -- and after the last iteration the per-rank gosa
+// partials (fp64) are summed.  Only the final iteration's gosa is observable
+// (jacobi returns it), so one reduction per jacobi call suffices.
+//
+// Transports:
+//  * in-process group (hp_group_jacobi): several slab contexts driven by one
+//    host thread; halo planes move by cudaMemcpyPeerAsync on the receiver's
+//    stream after a cross-stream event on the sender's stencil.  Used for one
+//    process driving several GPUs, and to test the decomposition with virtual
+//    ranks on a single GPU.
+//  * NCCL (hp_dd_*): one process per GPU; ncclSend/ncclRecv of the halo planes
+//    and one ncclAllReduce of gosa, on the context's stream.  libnccl.so.2 is
+//    dlopen'ed on first use (the library has no link-time NCCL dependency; an
+//    NCCL already loaded by torch is reused).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "context.h"
+
+using namespace hp;
+
+// ---------------------------------------------------------------- geometry
+
+extern "C" int hp_slab_range(int I, int nranks, int rank, int32_t* i_begin, int32_t* i_end) {
+  const int n = I - 3;  // interior planes [1, I-2)
+  if (I < 4 || nranks < 1 || rank < 0 || rank >= nranks || nranks > n || !i_begin || !i_end) {
+    set_error("hp_slab_range: bad arguments (I=%d nranks=%d rank=%d)", I, nranks, rank);
+    return HP_ERR_ARG;
+  }
+  *i_begin = 1 + (int)((long long)rank * n / nranks);
+  *i_end = 1 + (int)((long long)(rank + 1) * n / nranks);
+  return HP_OK;
+}
+
+extern "C" int hp_create_slab(int device, const hp_grid* global, int i_begin, int i_end,
+                              hp_ctx** out) {
+  if (!global || !out) {
+    set_error("hp_create_slab: null argument");
+    return HP_ERR_ARG;
+  }
+  *out = nullptr;
+  const int I = global->I;
+  if (I < 4 || global->J < 4 || global->K < 4 || i_begin < 1 || i_end > I - 2 ||
+      i_end <= i_begin) {
+    set_error("hp_create_slab: planes [%d, %d) not inside the interior of a %d-plane grid",
+              i_begin, i_end, I);
+    return HP_ERR_ARG;
+  }
+  hp_ctx* c = nullptr;
+  const int rc = create_ctx(device, i_end - i_begin + 2, global->J, global->K, &c);
+  if (rc != HP_OK) return rc;
+  c->gI = I;
+  c->i_off = i_begin - 1;
+  c->li_lo = 1;
+  c->li_hi = i_end - i_begin + 1;
+  *out = c;
+  return HP_OK;
+}
+
+namespace {
+
+size_t plane_bytes(const hp_ctx* c) { return c->dev.plane() * sizeof(float); }
+float* plane_ptr(hp_ctx* c, float* buf, int li) { return buf + (size_t)li * c->dev.plane(); }
+
+}  // namespace
+
+// ------------------------------------------------------- in-process group
+
+extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
+  if (!ctxs || n < 1 || nn < 0) {
+    set_error("hp_group_jacobi: bad arguments");
+    return HP_ERR_ARG;
+  }
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r]) {
+      set_error("hp_group_jacobi: null context %d", r);
+      return HP_ERR_ARG;
+    }
+    if (r > 0 && ctxs[r]->i_off + ctxs[r]->li_lo != ctxs[r - 1]->i_off + ctxs[r - 1]->li_hi) {
+      set_error("hp_group_jacobi: slab %d does not continue slab %d", r, r - 1);
+      return HP_ERR_ARG;
+    }
+  }
+  std::vector<cudaEvent_t> done(n, nullptr);
+  int rc = HP_OK;
+  auto fail = [&](cudaError_t e, const char* what) {
+    if (rc == HP_OK) rc = cuda_fail(e, what);
+  };
+  for (int r = 0; r < n && rc == HP_OK; ++r) {
+    cudaSetDevice(ctxs[r]->device);
+    cudaError_t e = cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming);
+    if (e != cudaSuccess) fail(e, "event create");
+    else if (time_loop_begin(ctxs[r], ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "begin");
+  }
+  for (int it = 0; it < nn && rc == HP_OK; ++it) {
+    for (int r = 0; r < n && rc == HP_OK; ++r) {
+      hp_ctx* c = ctxs[r];
+      cudaSetDevice(c->device);
+      if (time_loop_step(c, it, ctx_args(c, 1)) < 0) fail(cudaGetLastError(), "stencil");
+      c->launches++;
+      cudaError_t e = cudaEventRecord(done[r], c->stream);
+      if (e != cudaSuccess) fail(e, "event record");
+    }
+    for (int r = 0; r < n && rc == HP_OK; ++r) {
+      hp_ctx* c = ctxs[r];
+      cudaSetDevice(c->device);
+      float* out = time_loop_buffer(c, it + 1);
+      for (int side = -1; side <= 1 && rc == HP_OK; side += 2) {
+        const int q = r + side;
+        if (q < 0 || q >= n) continue;
+        hp_ctx* nb = ctxs[q];
+        float* nb_out = time_loop_buffer(nb, it + 1);
+        // lower halo <- neighbour's last interior plane; upper halo <- its first
+        const int dst_plane = side < 0 ? c->li_lo - 1 : c->li_hi;
+        const int src_plane = side < 0 ? nb->li_hi - 1 : nb->li_lo;
+        cudaError_t e = cudaStreamWaitEvent(c->stream, done[q], 0);
+        if (e == cudaSuccess)
+          e = cudaMemcpyPeerAsync(plane_ptr(c, out, dst_plane), c->device,
+                                  plane_ptr(nb, nb_out, src_plane), nb->device, plane_bytes(c),
+                                  c->stream);
+        if (e != cudaSuccess) fail(e, "halo copy");
+      }
+    }
+  }
+  for (int r = 0; r < n && rc == HP_OK; ++r) {
+    cudaSetDevice(ctxs[r]->device);
+    if (time_loop_end(ctxs[r], nn, ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "end");
+  }
+  // gosa of the last iteration: sum of the per-slab fp64 partials, in rank order
+  double total = 0.0;
+  for (int r = 0; r < n && rc == HP_OK; ++r) {
+    hp_ctx* c = ctxs[r];
+    cudaSetDevice(c->device);
+    double part = 0.0;
+    cudaError_t e = cudaMemcpyAsync(&part, c->dscal + HP_V_GOSA * SLOT_BYTES, sizeof(double),
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) fail(e, "gosa partial");
+    total += nn > 0 ? part : 0.0;
+  }
+  for (int r = 0; r < n; ++r)
+    if (done[r]) cudaEventDestroy(done[r]);
+  if (rc == HP_OK && gosa_out) *gosa_out = total;
+  return rc;
+}
+
+// ----------------------------------------------------------------- NCCL
+
+namespace {
+
+struct Nccl {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl* nccl() {
+  static Nccl lib;
+  static bool tried = false;
+  if (tried) return lib.handle ? &lib : nullptr;
+  tried = true;
+  // prefer an NCCL the process already loaded (torch's), else the system one
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  lib.GetUniqueId = reinterpret_cast<decltype(lib.GetUniqueId)>(sym("ncclGetUniqueId"));
+  lib.CommInitRank = reinterpret_cast<decltype(lib.CommInitRank)>(sym("ncclCommInitRank"));
+  lib.CommDestroy = reinterpret_cast<decltype(lib.CommDestroy)>(sym("ncclCommDestroy"));
+  lib.GroupStart = reinterpret_cast<decltype(lib.GroupStart)>(sym("ncclGroupStart"));
+  lib.GroupEnd = reinterpret_cast<decltype(lib.GroupEnd)>(sym("ncclGroupEnd"));
+  lib.Send = reinterpret_cast<decltype(lib.Send)>(sym("ncclSend"));
+  lib.Recv = reinterpret_cast<decltype(lib.Recv)>(sym("ncclRecv"));
+  lib.AllReduce = reinterpret_cast<decltype(lib.AllReduce)>(sym("ncclAllReduce"));
+  lib.GetErrorString = reinterpret_cast<decltype(lib.GetErrorString)>(sym("ncclGetErrorString"));
+  if (!lib.GetUniqueId || !lib.CommInitRank || !lib.CommDestroy || !lib.GroupStart ||
+      !lib.GroupEnd || !lib.Send || !lib.Recv || !lib.AllReduce || !lib.GetErrorString)
+    return nullptr;
+  lib.handle = h;
+  return &lib;
+}
+
+struct DD {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  set_error("%s: %s", what, nccl() ? nccl()->GetErrorString(r) : "nccl unavailable");
+  return HP_ERR_DEVICE;
+}
+
+}  // namespace
+
+void hp::dd_destroy(hp_ctx* c) {
+  DD* d = static_cast<DD*>(c->dd);
+  if (d && d->comm && nccl()) nccl()->CommDestroy(d->comm);
+  delete d;
+  c->dd = nullptr;
+}
+
+extern "C" int hp_nccl_unique_id(unsigned char* out, size_t n) {
+  if (!out || n < NCCL_UNIQUE_ID_BYTES) {
+    set_error("hp_nccl_unique_id: need %d bytes", NCCL_UNIQUE_ID_BYTES);
+    return HP_ERR_ARG;
+  }
+  Nccl* l = nccl();
+  if (!l) {
+    set_error("libnccl.so.2 not available");
+    return HP_ERR_DEVICE;
+  }
+  ncclUniqueId id;
+  const ncclResult_t r = l->GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return HP_OK;
+}
+
+extern "C" int hp_dd_init(hp_ctx* c, int nranks, int rank, const unsigned char* id, size_t n) {
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && (!id || n < 128))) {
+    set_error("hp_dd_init: bad arguments");
+    return HP_ERR_ARG;
+  }
+  if (c->dd) dd_destroy(c);
+  DD* d = new DD;
+  d->nranks = nranks;
+  d->rank = rank;
+  if (nranks > 1) {
+    Nccl* l = nccl();
+    if (!l) {
+      delete d;
+      set_error("libnccl.so.2 not available");
+      return HP_ERR_DEVICE;
+    }
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+    cudaSetDevice(c->device);
+    const ncclResult_t r = l->CommInitRank(&d->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      delete d;
+      return nccl_fail(r, "ncclCommInitRank");
+    }
+  }
+  c->dd = d;
+  return HP_OK;
+}
+
+// nn iterations with halo exchange after each, then the gosa all-reduce; async on hp_stream.
+extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
+  if (!c || !c->dd || nn < 0) {
+    set_error("hp_dd_jacobi: context not initialised for decomposition");
+    return HP_ERR_ARG;
+  }
+  DD* d = static_cast<DD*>(c->dd);
+  Nccl* l = d->nranks > 1 ? nccl() : nullptr;
+  cudaSetDevice(c->device);
+  const LaunchArgs a = ctx_args(c, 1);
+  if (time_loop_begin(c, a) < 0) return cuda_fail(cudaGetLastError(), "begin");
+  const size_t count = c->dev.plane();
+  for (int it = 0; it < nn; ++it) {
+    if (time_loop_step(c, it, a) < 0) return cuda_fail(cudaGetLastError(), "stencil");
+    c->launches++;
+    if (!l) continue;
+    float* out = time_loop_buffer(c, it + 1);
+    ncclResult_t r = l->GroupStart();
+    if (d->rank > 0) {
+      if (r == ncclSuccess)
+        r = l->Send(plane_ptr(c, out, c->li_lo), count, ncclFloat32, d->rank - 1, d->comm,
+                    c->stream);
+      if (r == ncclSuccess)
+        r = l->Recv(plane_ptr(c, out, c->li_lo - 1), count, ncclFloat32, d->rank - 1, d->comm,
+                    c->stream);
+    }
+    if (d->rank < d->nranks - 1) {
+      if (r == ncclSuccess)
+        r = l->Send(plane_ptr(c, out, c->li_hi - 1), count, ncclFloat32, d->rank + 1, d->comm,
+                    c->stream);
+      if (r == ncclSuccess)
+        r = l->Recv(plane_ptr(c, out, c->li_hi), count, ncclFloat32, d->rank + 1, d->comm,
+                    c->stream);
+    }
+    const ncclResult_t r2 = l->GroupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "halo exchange");
+    if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+  }
+  if (time_loop_end(c, nn, a) < 0) return cuda_fail(cudaGetLastError(), "end");
+  if (l && nn > 0) {
+    double* g = reinterpret_cast<double*>(c->dscal + HP_V_GOSA * SLOT_BYTES);
+    const ncclResult_t r = l->AllReduce(g, g, 1, ncclFloat64, ncclSum, d->comm, c->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "gosa all-reduce");
+  }
+  return HP_OK;
+}
+
+extern "C" int hp_dd_time_steps(hp_ctx* c, int steps, int nn, double* ms_out) {
+  if (!c || !ms_out || steps < 0) {
+    set_error("hp_dd_time_steps: bad arguments");
+    return HP_ERR_ARG;
+  }
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaEventRecord(c->ev0, c->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "event record");
+  for (int s = 0; s < steps; ++s) {
+    const int rc = hp_dd_jacobi(c, nn);
+    if (rc != HP_OK) return rc;
+  }
+  if ((e = cudaEventRecord(c->ev1, c->stream)) != cudaSuccess) return cuda_fail(e, "event record");
+  if ((e = cudaEventSynchronize(c->ev1)) != cudaSuccess) return cuda_fail(e, "event sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  *ms_out = ms;
+  return HP_OK;
+}

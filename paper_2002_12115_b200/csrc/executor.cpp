@@ -37,8 +37,7 @@
 #include <string>
 #include <vector>
 
-#include "coherence.h"
-#include "hp_internal.h"
+#include "context.h"
 
 using namespace hp;
 
@@ -46,7 +45,7 @@ using namespace hp;
 
 static thread_local std::string g_last_error;
 
-static void set_error(const char* fmt, ...) {
+void hp::set_error(const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -70,8 +69,6 @@ extern "C" int hp_device_count(void) {
 // --------------------------------------------------------- program tables
 
 namespace {
-
-enum { SLOT_BYTES = 8 };
 
 struct VarInfo {
   const char* name;
@@ -121,50 +118,33 @@ size_t round_up(size_t x, size_t q) { return (x + q - 1) / q * q; }
 
 // ------------------------------------------------------------------ context
 
-struct hp_ctx {
-  int device = 0;
-  int I = 0, J = 0, K = 0, P = 0;
-  size_t field_elems = 0;        // I*J*P
-  size_t field_stride = 0;       // slab offset between fields (2 MiB aligned)
-  cudaStream_t stream = nullptr;
-  float* slab = nullptr;         // HP_NFIELDS + 1 (rotation scratch) fields
-  DevFields dev{};
-  float* scratch = nullptr;      // rotation buffer for the fused time loop
-  float* host[HP_NFIELDS] = {};  // pinned [I][J][K]
-  unsigned char* hscal = nullptr;   // pinned scalar slots
-  unsigned char* dscal = nullptr;   // device scalar slots
-  double* partials = nullptr;
-  unsigned int* ticket = nullptr;
-  int capacity = 0;
-  std::vector<int32_t> samples;  // i,j,k triples
-  // per-run data-manager state
-  uint64_t clock = 0;
-  uint64_t host_ver[HP_NVARS] = {}, dev_ver[HP_NVARS] = {};
-  bool declared[HP_NVARS] = {};
-  int refcount[HP_NVARS] = {};
-  bool host_dirty[HP_NFIELDS] = {};  // written since the last fresh-process reset
-  Coherence coh[HP_NVARS];           // arrays: which side holds the latest data where
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  uint64_t launches = 0;         // kernels launched by this context (all entry points)
-
-  GosaSink sink() const {
-    GosaSink g;
-    g.slot = reinterpret_cast<double*>(dscal + HP_V_GOSA * SLOT_BYTES);
-    g.partials = partials;
-    g.ticket = ticket;
-    g.capacity = capacity;
-    return g;
+// p -> scratch -> p ... ; faces of scratch mirror p's; the final interior goes
+// to p (if it ended in scratch) and to wrk2, so p/wrk2/gosa match the unfused loop.
+float* hp::time_loop_buffer(hp_ctx* c, int it) {
+  return (it & 1) ? c->scratch : c->dev.f[HP_F_P];
+}
+int hp::time_loop_begin(hp_ctx* c, const LaunchArgs& a) {
+  return launch_copy_halo(c->dev, c->dev.f[HP_F_P], c->scratch, a, c->stream);
+}
+int hp::time_loop_step(hp_ctx* c, int it, const LaunchArgs& a) {
+  return launch_stencil_rotate(c->dev, time_loop_buffer(c, it), time_loop_buffer(c, it + 1), a,
+                               c->sink(), c->stream);
+}
+int hp::time_loop_end(hp_ctx* c, int nn, const LaunchArgs& a) {
+  float* last = time_loop_buffer(c, nn);
+  int n = 0, r;
+  if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a, c->stream)) < 0)
+    return -1;
+  n += r;
+  if (last != c->dev.f[HP_F_P]) {
+    if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a, c->stream)) < 0)
+      return -1;
+    n += r;
   }
-  HostFields hostf() const {
-    HostFields h;
-    for (int f = 0; f < HP_NFIELDS; ++f) h.f[f] = host[f];
-    h.I = I; h.J = J; h.K = K;
-    return h;
-  }
-  template <class T> T& hs(int v) { return *reinterpret_cast<T*>(hscal + v * SLOT_BYTES); }
-};
+  return n;
+}
 
-static int cuda_fail(cudaError_t e, const char* what) {
+int hp::cuda_fail(cudaError_t e, const char* what) {
   set_error("%s: %s", what, cudaGetErrorString(e));
   return e == cudaErrorMemoryAllocation ? HP_ERR_OOM : HP_ERR_DEVICE;
 }
@@ -181,6 +161,7 @@ extern "C" void hp_destroy(hp_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->dd) dd_destroy(c);
   if (c->dev.tma) destroy_stencil_tma(const_cast<void*>(c->dev.tma));
   if (c->slab) cudaFree(c->slab);
   if (c->dscal) cudaFree(c->dscal);
@@ -204,6 +185,11 @@ extern "C" int hp_create(int device, const hp_grid* grid, int flags, hp_ctx** ou
     set_error("hp_create: extents must be >= 4 (got %d x %d x %d)", grid->I, grid->J, grid->K);
     return HP_ERR_ARG;
   }
+  return hp::create_ctx(device, grid->I, grid->J, grid->K, out);
+}
+
+int hp::create_ctx(int device, int I, int J, int K, hp_ctx** out) {
+  *out = nullptr;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -221,7 +207,8 @@ extern "C" int hp_create(int device, const hp_grid* grid, int flags, hp_ctx** ou
     return HP_ERR_OOM;
   }
   c->device = device;
-  c->I = grid->I; c->J = grid->J; c->K = grid->K;
+  c->I = I; c->J = J; c->K = K;
+  c->gI = c->I; c->i_off = 0; c->li_lo = 1; c->li_hi = c->I - 2;
   c->P = (int)round_up((size_t)c->K + 4, kRowAlign);
   c->field_elems = (size_t)c->I * c->J * c->P;
   c->field_stride = round_up(c->field_elems, (size_t)1 << 19);  // 2 MiB of floats
@@ -595,13 +582,8 @@ struct Runner {
 
   // --- kernel launches ---------------------------------------------------------
   LaunchArgs args(int reset) const {
-    LaunchArgs a;
-    a.imax = C->hs<int>(HP_V_IMAX);
-    a.jmax = C->hs<int>(HP_V_JMAX);
-    a.kmax = C->hs<int>(HP_V_KMAX);
-    a.omega = C->hs<float>(HP_V_OMEGA);
-    a.gosa_reset = reset;
-    return a;
+    return grid_args(C->hs<int>(HP_V_IMAX), C->hs<int>(HP_V_JMAX), C->hs<int>(HP_V_KMAX),
+                     C->hs<float>(HP_V_OMEGA), reset);
   }
 
   // implicit present_or_copy for arrays (and the gosa reduction scalar)
@@ -784,31 +766,15 @@ struct Runner {
 
  public:
   static int time_loop_fused(hp_ctx* c, int nn, const LaunchArgs& a) {
-    // p -> scratch -> p ... ; faces of scratch mirror p's; final interior goes
-    // to p (if it ended in scratch) and to wrk2.
-    float* bufs[2] = {c->dev.f[HP_F_P], c->scratch};
     int n = 0, r;
-    if ((r = launch_copy_halo(c->dev, bufs[0], bufs[1], a.imax, a.jmax, a.kmax, c->stream)) < 0)
-      return -1;
+    if ((r = time_loop_begin(c, a)) < 0) return -1;
     n += r;
     for (int it = 0; it < nn; ++it) {
-      if ((r = launch_stencil_rotate(c->dev, bufs[it & 1], bufs[(it + 1) & 1], a, c->sink(),
-                                     c->stream)) < 0)
-        return -1;
+      if ((r = time_loop_step(c, it, a)) < 0) return -1;
       n += r;
     }
-    float* last = bufs[nn & 1];
-    if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a.imax, a.jmax,
-                                         a.kmax, c->stream)) < 0)
-      return -1;
-    n += r;
-    if (last != c->dev.f[HP_F_P]) {
-      if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a.imax, a.jmax,
-                                           a.kmax, c->stream)) < 0)
-        return -1;
-      n += r;
-    }
-    return n;
+    if ((r = time_loop_end(c, nn, a)) < 0) return -1;
+    return n + r;
   }
 
   void run_time_loop() {
@@ -1043,15 +1009,7 @@ extern "C" int hp_read_gosa(hp_ctx* c, int side, double* out) {
 
 // ------------------------------------------------- device-resident Jacobi
 
-static LaunchArgs default_args(const hp_ctx* c, int reset) {
-  LaunchArgs a;
-  a.imax = c->I - 1;
-  a.jmax = c->J - 1;
-  a.kmax = c->K - 1;
-  a.omega = 0.8f;
-  a.gosa_reset = reset;
-  return a;
-}
+static LaunchArgs default_args(const hp_ctx* c, int reset) { return ctx_args(c, reset); }
 
 extern "C" int hp_launches_per_iteration(int variant) { return variant == 1 ? 1 : 2; }
 
@@ -1061,7 +1019,8 @@ extern "C" int hp_init_device(hp_ctx* c) {
   const LaunchArgs a = default_args(c, 0);
   GosaSink g = c->sink();
   Box b0{0, c->I, 0, c->J, 0, c->K};
-  Box b1{0, a.imax, 0, a.jmax, 0, a.kmax};
+  // initmt nest B over global i < imax: local planes [0, imax - i_off)
+  Box b1{0, std::min(c->I, a.imax - c->i_off), 0, a.jmax, 0, a.kmax};
   if (launch_fill(c->dev.f[HP_F_WRK2], c->field_elems, 0.0f, c->stream) < 0 ||
       launch_nest(NEST_INIT0, MAP_COLLAPSE, c->dev, b0, a, g, c->stream) < 0 ||
       launch_nest(NEST_INIT1, MAP_COLLAPSE, c->dev, b1, a, g, c->stream) < 0)
@@ -1144,7 +1103,7 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
   bool ok = mark();
   float* bufs[2] = {c->dev.f[HP_F_P], c->scratch};
   if (variant == 1) {
-    ok = ok && launch_copy_halo(c->dev, bufs[0], bufs[1], a.imax, a.jmax, a.kmax, c->stream) >= 0;
+    ok = ok && launch_copy_halo(c->dev, bufs[0], bufs[1], a, c->stream) >= 0;
     is_stencil.push_back(0);
     ok = ok && mark();
     for (int it = 0; ok && it < nn; ++it) {
@@ -1153,11 +1112,10 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
       is_stencil.push_back(1);
     }
     float* last = bufs[nn & 1];
-    ok = ok && launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a.imax, a.jmax,
-                                           a.kmax, c->stream) >= 0 && mark();
+    ok = ok && launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a, c->stream) >= 0 && mark();
     is_stencil.push_back(0);
     if (ok && last != c->dev.f[HP_F_P]) {
-      ok = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a.imax, a.jmax, a.kmax,
+      ok = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_P], a,
                                        c->stream) >= 0 && mark();
       is_stencil.push_back(0);
     }

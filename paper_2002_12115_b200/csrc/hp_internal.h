@@ -57,10 +57,20 @@ enum Mapping {
 };
 
 struct LaunchArgs {
-  int imax, jmax, kmax;                 // program scalars (by value)
+  int imax, jmax, kmax;                 // program scalars (by value; global grid)
   float omega;
   int gosa_reset;                       // stencil: store instead of accumulate
+  int i_off;                            // global i of local plane 0 (slab contexts)
+  int li_lo, li_hi;                     // local planes of the stencil interior
 };
+
+// Full-grid arguments: local == global planes, interior [1, imax-1).
+inline LaunchArgs grid_args(int imax, int jmax, int kmax, float omega, int reset) {
+  LaunchArgs a;
+  a.imax = imax; a.jmax = jmax; a.kmax = kmax; a.omega = omega; a.gosa_reset = reset;
+  a.i_off = 0; a.li_lo = 1; a.li_hi = imax - 1;
+  return a;
+}
 
 // ---- kernels.cu launchers (all enqueue on `s`, no host sync) ----------------
 // Returns number of kernels launched (>=0) or -1 on launch error.
@@ -75,12 +85,13 @@ int launch_copy_3d(const DevFields& F, const LaunchArgs& a, cudaStream_t s);
 int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
                           const LaunchArgs& a, const GosaSink& g, cudaStream_t s);
 int launch_fill(float* dst, size_t n, float value, cudaStream_t s);
-// dst = src on every point outside the stencil interior
-int launch_copy_halo(const DevFields& F, const float* src, float* dst, int imax, int jmax,
-                     int kmax, cudaStream_t s);
-// dst = src on the interior [1,imax-1) x [1,jmax-1) x [1,kmax-1)
-int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst, int imax,
-                                int jmax, int kmax, cudaStream_t s);
+// dst = src on every point outside the stencil interior (local planes outside
+// [li_lo, li_hi) included whole)
+int launch_copy_halo(const DevFields& F, const float* src, float* dst, const LaunchArgs& a,
+                     cudaStream_t s);
+// dst = src on the interior [li_lo,li_hi) x [1,jmax-1) x [1,kmax-1)
+int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst,
+                                const LaunchArgs& a, cudaStream_t s);
 int gosa_capacity_needed(const DevFields& F);
 // select the tuned-stencil configuration; returns the number of configs or -1
 int set_stencil_config(int cfg);

@@ -113,7 +113,7 @@ __device__ __forceinline__ void nest_point(const DevFields& F, int i, int j, int
   if (NEST == NEST_INIT0) {
     body_init0(F, c);
   } else if (NEST == NEST_INIT1) {
-    body_init1(F, c, i, a.imax);
+    body_init1(F, c, i + a.i_off, a.imax);
   } else if (NEST == NEST_STENCIL) {
     body_stencil(F, F.f[HP_F_P], F.f[HP_F_WRK2], c, a.omega, acc);
   } else {
@@ -368,13 +368,13 @@ k_copy_3d(DevFields F, const float* __restrict__ src, float* __restrict__ dst,
 // reads but never writes): whole rows on boundary planes/rows, else the row
 // ends k = 0 and k >= kmax-1.  One thread per (i, j) row.
 __global__ void k_copy_halo(DevFields F, const float* __restrict__ src, float* __restrict__ dst,
-                            int imax, int jmax, int kmax) {
+                            int li_lo, int li_hi, int jmax, int kmax) {
   const long long rows = (long long)F.I * F.J;
   for (long long r = (long long)blockIdx.x * blockDim.y + threadIdx.y; r < rows;
        r += (long long)gridDim.x * blockDim.y) {
     const int i = (int)(r / F.J), j = (int)(r % F.J);
     const size_t base = F.at(i, j, 0);
-    const bool whole = i == 0 || i >= imax - 1 || j == 0 || j >= jmax - 1;
+    const bool whole = i < li_lo || i >= li_hi || j == 0 || j >= jmax - 1;
     if (whole) {
       for (int k = threadIdx.x; k < F.K; k += blockDim.x) dst[base + k] = src[base + k];
     } else {
@@ -483,7 +483,7 @@ int set_stencil_config(int cfg) {
 
 int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
                           const LaunchArgs& a, const GosaSink& g, cudaStream_t s) {
-  const int i_lo = 1, i_hi = a.imax - 1, j_lo = 1, j_hi = a.jmax - 1;
+  const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1;
   const int k_lo = 1, k_hi = a.kmax - 1;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) {
     // empty interior: the nest body never runs, gosa keeps (or resets to) 0
@@ -513,9 +513,10 @@ int launch_stencil_3d(const DevFields& F, const LaunchArgs& a, const GosaSink& g
   return launch_stencil_rotate(F, F.f[HP_F_P], F.f[HP_F_WRK2], a, g, s);
 }
 
-static int copy_interior_impl(const DevFields& F, const float* src, float* dst, int imax,
-                              int jmax, int kmax, cudaStream_t s) {
-  const int i_lo = 1, i_hi = imax - 1, j_lo = 1, j_hi = jmax - 1, k_lo = 1, k_hi = kmax - 1;
+static int copy_interior_impl(const DevFields& F, const float* src, float* dst,
+                              const LaunchArgs& a, cudaStream_t s) {
+  const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
+            k_hi = a.kmax - 1;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   const long long total = (long long)(i_hi - i_lo) * (j_hi - j_lo) * ((k_hi + 3) / 4);
   long long blocks = (total + 255) / 256;
@@ -526,12 +527,13 @@ static int copy_interior_impl(const DevFields& F, const float* src, float* dst, 
 }
 
 int launch_copy_3d(const DevFields& F, const LaunchArgs& a, cudaStream_t s) {
-  return copy_interior_impl(F, F.f[HP_F_WRK2], F.f[HP_F_P], a.imax, a.jmax, a.kmax, s);
+  return copy_interior_impl(F, F.f[HP_F_WRK2], F.f[HP_F_P], a, s);
 }
 
-int launch_copy_halo(const DevFields& F, const float* src, float* dst, int imax, int jmax,
-                     int kmax, cudaStream_t s) {
-  k_copy_halo<<<sm_count() * 4, dim3(64, 4), 0, s>>>(F, src, dst, imax, jmax, kmax);
+int launch_copy_halo(const DevFields& F, const float* src, float* dst, const LaunchArgs& a,
+                     cudaStream_t s) {
+  k_copy_halo<<<sm_count() * 4, dim3(64, 4), 0, s>>>(F, src, dst, a.li_lo, a.li_hi, a.jmax,
+                                                     a.kmax);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -541,9 +543,9 @@ int launch_fill(float* dst, size_t n, float value, cudaStream_t s) {
 }
 
 // interior copy between arbitrary buffers with the program's interior bounds
-int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst, int imax,
-                                int jmax, int kmax, cudaStream_t s) {
-  return copy_interior_impl(F, src, dst, imax, jmax, kmax, s);
+int launch_copy_interior_bounds(const DevFields& F, const float* src, float* dst,
+                                const LaunchArgs& a, cudaStream_t s) {
+  return copy_interior_impl(F, src, dst, a, s);
 }
 
 }  // namespace hp

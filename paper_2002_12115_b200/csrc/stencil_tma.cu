@@ -309,7 +309,7 @@ bool encode(CUtensorMap* m, const DevFields& F, const float* base, uint32_t box_
   const cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
@@ -352,7 +352,8 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
                        int sms) {
   const TmaState* t = static_cast<const TmaState*>(h);
   if (!t || (p_in != t->p && p_in != t->scratch)) return 0;
-  const int i_lo = 1, i_hi = a.imax - 1, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1, k_hi = a.kmax - 1;
+  const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
+            k_hi = a.kmax - 1;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   StencilMaps maps = t->base;
   if (p_in == t->scratch) maps.pin = t->scratch_map;

@@ -103,6 +103,14 @@ SIGNATURES = {
     "hp_time_jacobi": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(KernelTimes)]),
     "hp_launch_count": (C.c_uint64, [_CtxP]),
     "hp_set_stencil_config": (C.c_int, [C.c_int]),
+    "hp_slab_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32)]),
+    "hp_create_slab": (C.c_int, [C.c_int, C.POINTER(Grid), C.c_int, C.c_int, C.POINTER(_CtxP)]),
+    "hp_group_jacobi": (C.c_int, [C.POINTER(_CtxP), C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "hp_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "hp_dd_init": (C.c_int, [_CtxP, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
+    "hp_dd_jacobi": (C.c_int, [_CtxP, C.c_int]),
+    "hp_dd_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "hp_host_alloc": (C.c_void_p, [C.c_size_t]),
     "hp_host_free": (None, [C.c_void_p]),
 }
@@ -139,6 +147,20 @@ def load(path=None):
         return lib
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(load().hp_nccl_unique_id(buf, 128), "hp_nccl_unique_id")
+    return buf.raw
+
+
+def group_jacobi(contexts, nn: int) -> float:
+    """Drive slab contexts in-process for nn iterations; returns the global gosa."""
+    arr = (C.c_void_p * len(contexts))(*[c.ptr.value for c in contexts])
+    g = C.c_double()
+    check(load().hp_group_jacobi(arr, len(contexts), nn, C.byref(g)), "hp_group_jacobi")
+    return g.value
+
+
 def last_error() -> str:
     msg = load().hp_last_error()
     return msg.decode(errors="replace") if msg else ""
@@ -157,16 +179,33 @@ def check(rc: int, what: str) -> int:
     return rc
 
 
-class Context:
-    """One device context (one evaluator worker / one GPU)."""
+def slab_range(I: int, nranks: int, rank: int) -> tuple:
+    """Interior planes [i_begin, i_end) of `rank` (C: hp_slab_range)."""
+    b, e = C.c_int32(), C.c_int32()
+    check(load().hp_slab_range(I, nranks, rank, C.byref(b), C.byref(e)), "hp_slab_range")
+    return b.value, e.value
 
-    def __init__(self, device: int, I: int, J: int, K: int):
+
+class Context:
+    """One device context (one evaluator worker / one GPU), or one slab of a grid."""
+
+    def __init__(self, device: int, I: int, J: int, K: int, slab=None):
         self.lib = load()
         self.device = device
-        self.shape = (I, J, K)
         ptr = C.c_void_p()
-        check(self.lib.hp_create(device, C.byref(Grid(I, J, K)), 0, C.byref(ptr)),
-              f"hp_create(device={device}, {I}x{J}x{K})")
+        if slab is None:
+            self.shape = (I, J, K)
+            self.i_off = 0
+            check(self.lib.hp_create(device, C.byref(Grid(I, J, K)), 0, C.byref(ptr)),
+                  f"hp_create(device={device}, {I}x{J}x{K})")
+        else:
+            i_begin, i_end = slab
+            self.shape = (i_end - i_begin + 2, J, K)
+            self.i_off = i_begin - 1
+            check(self.lib.hp_create_slab(device, C.byref(Grid(I, J, K)), i_begin, i_end,
+                                          C.byref(ptr)),
+                  f"hp_create_slab(device={device}, planes [{i_begin},{i_end}) of {I})")
+        self.global_shape = (I, J, K)
         self._ptr = ptr
 
     @property
@@ -248,6 +287,18 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(self.lib.hp_launch_count(self.ptr))
+
+    def dd_init(self, nranks: int, rank: int, uid: bytes = b"") -> None:
+        buf = C.create_string_buffer(bytes(uid), max(128, len(uid)))
+        check(self.lib.hp_dd_init(self.ptr, nranks, rank, buf, len(uid)), "hp_dd_init")
+
+    def dd_jacobi(self, nn: int) -> None:
+        check(self.lib.hp_dd_jacobi(self.ptr, nn), "hp_dd_jacobi")
+
+    def dd_time_steps(self, steps: int, nn: int) -> float:
+        ms = C.c_double()
+        check(self.lib.hp_dd_time_steps(self.ptr, steps, nn, C.byref(ms)), "hp_dd_time_steps")
+        return ms.value
 
     def jacobi_host(self, fields: dict, nn: int, variant: int, p_out) -> float:
         """fields: name -> contiguous float32 [I,J,K] host arrays (numpy); p_out likewise."""

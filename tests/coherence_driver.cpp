@@ -64,6 +64,18 @@ int main() {
   CHECK(c.log.size() == 1 && vol(c.region(hp::OWN_HOST)) == full.count());
   c.all_synced(full);
   CHECK(c.region(hp::OWN_HOST).empty() && c.region(hp::OWN_DEV).empty());
+  // row-by-row writes (row kernels under host loops) coalesce into one slab
+  {
+    Coherence r;
+    r.reset(full);
+    for (int i = in.i0; i < in.i1; ++i)
+      for (int j = in.j0; j < in.j1; ++j) {
+        r.write(Box{i, i + 1, j, j + 1, in.k0, in.k1}, hp::OWN_DEV);
+        CHECK(r.log.size() <= 3);
+      }
+    CHECK(vol(r.region(hp::OWN_DEV)) == in.count());
+    CHECK(vol(r.region(hp::OWN_HOST)) == full.count() - in.count());
+  }
   std::printf("OK\n");
   return 0;
 }

@@ -1,0 +1,144 @@
+"""Slab decomposition: partition/halo logic on CPU (gloo, world_size 2-3) and on GPU.
+
+The CPU test runs the decomposition with host slabs: each gloo rank applies the
+stencil to its slab in numpy float32 (every op rounds like the C program), swaps
+halo planes with its neighbours exactly as hp_dd_jacobi does (dd.halo_plan), and
+all-reduces the fp64 gosa; the gathered field must equal the full-grid oracle.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle
+from paper_2002_12115_b200 import dd
+from paper_2002_12115_b200 import native as N
+from paper_2002_12115_b200.apps import himeno
+
+F32 = np.float32
+
+
+def stencil_slab(f, lo, hi, jmax, kmax, omega=F32(0.8)):
+    """Interior planes [lo, hi) of a slab (numpy float32, C evaluation order)."""
+    p = f["p"]
+    I_, J_, K_ = p.shape
+    i, j, k = slice(lo, hi), slice(1, jmax - 1), slice(1, kmax - 1)
+
+    def P(di, dj, dk):
+        return p[lo + di:hi + di, 1 + dj:jmax - 1 + dj, 1 + dk:kmax - 1 + dk]
+
+    c = (i, j, k)
+    s0 = f["a0"][c] * P(1, 0, 0) + f["a1"][c] * P(0, 1, 0) + f["a2"][c] * P(0, 0, 1) \
+        + f["b0"][c] * (P(1, 1, 0) - P(1, -1, 0) - P(-1, 1, 0) + P(-1, -1, 0)) \
+        + f["b1"][c] * (P(0, 1, 1) - P(0, -1, 1) - P(0, 1, -1) + P(0, -1, -1)) \
+        + f["b2"][c] * (P(1, 0, 1) - P(-1, 0, 1) - P(1, 0, -1) + P(-1, 0, -1)) \
+        + f["c0"][c] * P(-1, 0, 0) + f["c1"][c] * P(0, -1, 0) + f["c2"][c] * P(0, 0, -1) \
+        + f["wrk1"][c]
+    ss = (s0 * f["a3"][c] - P(0, 0, 0)) * f["bnd"][c]
+    out = p.copy()
+    out[c] = P(0, 0, 0) + omega * ss
+    assert out.dtype == F32
+    return out, float(np.sum((ss * ss).astype(np.float64)))
+
+
+def _rank_main(rank, world, name, nn, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sz = himeno.size(name)
+    full = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(full)
+    b, e = dd.slab_range(sz.I, world, rank)
+    f = {k: v[b - 1:e + 1].copy() for k, v in full.items()}
+    plan = {r: (s, rv) for r, s, rv in dd.halo_plan(sz.I, world)}
+    n = e - b
+    gosa = 0.0
+    for _ in range(nn):
+        f["p"], part = stencil_slab(f, 1, n + 1, sz.J - 1, sz.K - 1)
+        sends, recvs = plan[rank]
+        reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(f["p"][pl])), dst)
+                for dst, pl in sends]
+        for src, pl in recvs:
+            buf = torch.empty(f["p"][pl].shape, dtype=torch.float32)
+            dist.recv(buf, src)
+            f["p"][pl] = buf.numpy()
+        for r in reqs:
+            r.wait()
+        t = torch.tensor([part], dtype=torch.float64)
+        dist.all_reduce(t)
+        gosa = float(t.item())
+    pieces = [None] * world
+    dist.all_gather_object(pieces, (b, e, f["p"][1:-1]))
+    if rank == 0:
+        p = full["p"].copy()
+        for bb, ee, arr in pieces:
+            p[bb:ee] = arr
+        ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+        q.put((bool(np.array_equal(p, ref["fields"]["p"])), gosa, ref["gosa64"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_slab_decomposition_matches_oracle(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + world * 7 + os.getpid() % 1000
+    procs = [ctx.Process(target=_rank_main, args=(r, world, "XXS", 3, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    same, gosa, want = q.get(timeout=10)
+    assert same
+    assert abs(gosa - want) <= 1e-12 * want
+
+
+def test_slab_range_partition():
+    for I in (9, 33, 65, 257, 513):
+        for n in range(1, min(9, I - 3) + 1):
+            ranges = [dd.slab_range(I, n, r) for r in range(n)]
+            assert ranges[0][0] == 1 and ranges[-1][1] == I - 2
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            sizes = [e - b for b, e in ranges]
+            assert max(sizes) - min(sizes) <= 1
+            assert ranges == [N.slab_range(I, n, r) for r in range(n)]   # C ABI agrees
+    with pytest.raises(ValueError):
+        dd.slab_range(9, 7, 0)
+
+
+def test_halo_plan_is_symmetric():
+    for world in (2, 3, 8):
+        plan = dd.halo_plan(257, world)
+        sends = {(r, dst) for r, s, _ in plan for dst, _ in s}
+        recvs = {(src, r) for r, _, rv in plan for src, _ in rv}
+        assert sends == recvs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks", [1, 2, 3, 4])
+@pytest.mark.parametrize("name,nn", [("XS", 3), ("M", 2)])
+def test_gpu_group_slabs_match_oracle(gpu, ranks, name, nn):
+    """Virtual ranks on one GPU: decomposition is bit-exact with the full grid."""
+    sz = himeno.size(name)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    with dd.GroupJacobi(name, [0] * ranks) as g:
+        gosa = g.jacobi(nn)
+        p = g.gather("p")
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(gosa - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
+
+
+@pytest.mark.gpu
+def test_gpu_slab_single_rank_dd(gpu):
+    """hp_dd_* with world 1 (no NCCL): same result as the full grid."""
+    sz = himeno.size("XS")
+    ref = oracle.run_program(sz.I, sz.J, sz.K, 3)
+    s = dd.SlabJacobi("XS", 0, 1, 0)
+    s.jacobi(3)
+    assert abs(s.gosa() - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
+    assert np.array_equal(s.interior_p(), ref["fields"]["p"][1:sz.I - 2])
+    s.close()

@@ -77,6 +77,11 @@ int time_loop_step(hp_ctx* c, int it, const LaunchArgs& a);
 int time_loop_end(hp_ctx* c, int nn, const LaunchArgs& a);
 float* time_loop_buffer(hp_ctx* c, int it);   // buffer holding p after `it` steps
 void dd_destroy(hp_ctx* c);                   // decomp.cpp
+// Whole-field host <-> device copies: one contiguous PCIe transfer through the
+// rotation scratch buffer (staging) + an on-device repitch, instead of a
+// pitched 2-D copy of K-float rows.  Stream-ordered; `host` is [I][J][K].
+cudaError_t field_to_device(hp_ctx* c, float* dev_field, const float* host);
+cudaError_t field_to_host(hp_ctx* c, float* host, const float* dev_field);
 // allocate a context for a local I x J x K field set (no extent checks)
 int create_ctx(int device, int I, int J, int K, hp_ctx** out);
 void set_error(const char* fmt, ...);

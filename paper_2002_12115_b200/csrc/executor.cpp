@@ -118,6 +118,25 @@ size_t round_up(size_t x, size_t q) { return (x + q - 1) / q * q; }
 
 // ------------------------------------------------------------------ context
 
+cudaError_t hp::field_to_device(hp_ctx* c, float* dev_field, const float* host) {
+  const size_t n = (size_t)c->I * c->J * c->K;
+  cudaError_t e = cudaMemcpyAsync(c->scratch, host, n * sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream);
+  if (e != cudaSuccess) return e;
+  if (launch_repitch(dev_field, (size_t)c->P, c->scratch, (size_t)c->K, c->K,
+                     (size_t)c->I * c->J, c->stream) < 0)
+    return cudaGetLastError();
+  return cudaSuccess;
+}
+
+cudaError_t hp::field_to_host(hp_ctx* c, float* host, const float* dev_field) {
+  const size_t n = (size_t)c->I * c->J * c->K;
+  if (launch_repitch(c->scratch, (size_t)c->K, dev_field, (size_t)c->P, c->K,
+                     (size_t)c->I * c->J, c->stream) < 0)
+    return cudaGetLastError();
+  return cudaMemcpyAsync(host, c->scratch, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream);
+}
+
 // p -> scratch -> p ... ; faces of scratch mirror p's; the final interior goes
 // to p (if it ended in scratch) and to wrk2, so p/wrk2/gosa match the unfused loop.
 float* hp::time_loop_buffer(hp_ctx* c, int it) {
@@ -407,11 +426,8 @@ struct Runner {
     cudaError_t e;
     const size_t K4 = (size_t)C->K * sizeof(float), P4 = (size_t)C->P * sizeof(float);
     if (box_contains(b, full_box())) {
-      e = kind == cudaMemcpyHostToDevice
-              ? cudaMemcpy2DAsync(C->dev.f[fid], P4, C->host[fid], K4, K4, (size_t)C->I * C->J,
-                                  kind, C->stream)
-              : cudaMemcpy2DAsync(C->host[fid], K4, C->dev.f[fid], P4, K4, (size_t)C->I * C->J,
-                                  kind, C->stream);
+      e = kind == cudaMemcpyHostToDevice ? field_to_device(C, C->dev.f[fid], C->host[fid])
+                                         : field_to_host(C, C->host[fid], C->dev.f[fid]);
     } else {
       cudaMemcpy3DParms m = {};
       cudaPitchedPtr d = make_cudaPitchedPtr(C->dev.f[fid], P4, K4, (size_t)C->J);
@@ -963,10 +979,7 @@ extern "C" int hp_read_field(hp_ctx* c, int field, int side, float* dst, size_t 
     memcpy(dst, c->host[field], n * sizeof(float));
     return HP_OK;
   }
-  CK(cudaMemcpy2DAsync(dst, (size_t)c->K * sizeof(float), c->dev.f[field],
-                       (size_t)c->P * sizeof(float), (size_t)c->K * sizeof(float),
-                       (size_t)c->I * c->J, cudaMemcpyDeviceToHost, c->stream),
-     "read field");
+  CK(field_to_host(c, dst, c->dev.f[field]), "read field");
   CK(cudaStreamSynchronize(c->stream), "read field sync");
   return HP_OK;
 }
@@ -982,10 +995,7 @@ extern "C" int hp_write_field(hp_ctx* c, int field, int side, const float* src, 
     c->host_dirty[field] = true;
     return HP_OK;
   }
-  CK(cudaMemcpy2DAsync(c->dev.f[field], (size_t)c->P * sizeof(float), src,
-                       (size_t)c->K * sizeof(float), (size_t)c->K * sizeof(float),
-                       (size_t)c->I * c->J, cudaMemcpyHostToDevice, c->stream),
-     "write field");
+  CK(field_to_device(c, c->dev.f[field], src), "write field");
   CK(cudaStreamSynchronize(c->stream), "write field sync");
   return HP_OK;
 }
@@ -1162,17 +1172,11 @@ extern "C" int hp_jacobi_host(hp_ctx* c, const float* const* fields, int nn, int
       set_error("hp_jacobi_host: field %d missing", f);
       return HP_ERR_ARG;
     }
-    CK(cudaMemcpy2DAsync(c->dev.f[f], (size_t)c->P * sizeof(float), fields[f],
-                         (size_t)c->K * sizeof(float), (size_t)c->K * sizeof(float),
-                         (size_t)c->I * c->J, cudaMemcpyHostToDevice, c->stream),
-       "jacobi H2D");
+    CK(field_to_device(c, c->dev.f[f], fields[f]), "jacobi H2D");
   }
   int rc = hp_jacobi_device(c, nn, variant);
   if (rc != HP_OK) return rc;
-  CK(cudaMemcpy2DAsync(p_out, (size_t)c->K * sizeof(float), c->dev.f[HP_F_P],
-                       (size_t)c->P * sizeof(float), (size_t)c->K * sizeof(float),
-                       (size_t)c->I * c->J, cudaMemcpyDeviceToHost, c->stream),
-     "jacobi D2H p");
+  CK(field_to_host(c, p_out, c->dev.f[HP_F_P]), "jacobi D2H p");
   CK(cudaMemcpyAsync(gosa_out, c->dscal + HP_V_GOSA * SLOT_BYTES, sizeof(double),
                      cudaMemcpyDeviceToHost, c->stream),
      "jacobi D2H gosa");

@@ -85,6 +85,9 @@ int launch_copy_3d(const DevFields& F, const LaunchArgs& a, cudaStream_t s);
 int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
                           const LaunchArgs& a, const GosaSink& g, cudaStream_t s);
 int launch_fill(float* dst, size_t n, float value, cudaStream_t s);
+// dst[r*dpitch + c] = src[r*spitch + c] for r < rows, c < width (elements)
+int launch_repitch(float* dst, size_t dpitch, const float* src, size_t spitch, int width,
+                   size_t rows, cudaStream_t s);
 // dst = src on every point outside the stencil interior (local planes outside
 // [li_lo, li_hi) included whole)
 int launch_copy_halo(const DevFields& F, const float* src, float* dst, const LaunchArgs& a,

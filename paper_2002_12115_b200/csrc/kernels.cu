@@ -384,6 +384,17 @@ __global__ void k_copy_halo(DevFields F, const float* __restrict__ src, float* _
   }
 }
 
+// 2-D copy between row pitches (elements): host-layout staging <-> pitched field
+__global__ void k_repitch(float* __restrict__ dst, size_t dpitch, const float* __restrict__ src,
+                          size_t spitch, int width, size_t rows) {
+  const size_t total = rows * (size_t)width;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = t / (size_t)width, c = t % (size_t)width;
+    dst[r * dpitch + c] = src[r * spitch + c];
+  }
+}
+
 __global__ void k_fill(float* dst, size_t n, float v) {
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (size_t)gridDim.x * blockDim.x)
@@ -534,6 +545,12 @@ int launch_copy_halo(const DevFields& F, const float* src, float* dst, const Lau
                      cudaStream_t s) {
   k_copy_halo<<<sm_count() * 4, dim3(64, 4), 0, s>>>(F, src, dst, a.li_lo, a.li_hi, a.jmax,
                                                      a.kmax);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_repitch(float* dst, size_t dpitch, const float* src, size_t spitch, int width,
+                   size_t rows, cudaStream_t s) {
+  k_repitch<<<sm_count() * 8, 256, 0, s>>>(dst, dpitch, src, spitch, width, rows);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

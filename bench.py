@@ -257,9 +257,11 @@ def run_ours(args, world, rank, local):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_stencil_tma<3> (TMA ring; fused time loop)" if variant == 1 else "k_stencil_tma<3>",
+                "kernel": ("k_stencil_tb2 (TMA ring, 2 iterations per pass; fused time loop)"
+                           if variant == 1 and kt.stencil_iters > 1.5 else "k_stencil_tma<3>"),
                 "bytes_per_point": BYTES_STENCIL, "points_per_launch": points,
                 "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,
+                "iterations_per_launch": kt.stencil_iters,
                 "peak_source": peak_src}
 
     # e2e through the C ABI with pinned host buffers: H2D of the inputs, the

@@ -200,8 +200,9 @@ int hp_launches_per_iteration(int variant);
  * the mean duration of the stencil launches and of the other launches. */
 typedef struct hp_kernel_times {
   double total_ms;        /* first to last event of the call                 */
-  double stencil_ms;      /* mean duration of one stencil launch              */
+  double stencil_ms;      /* mean duration of one stencil launch (pass)       */
   double other_ms;        /* mean duration of the other launches (copies)     */
+  double stencil_iters;   /* mean Jacobi iterations per stencil pass (1 or 2) */
   int32_t n_stencil, n_other;
 } hp_kernel_times;
 int hp_time_steps(hp_ctx* ctx, int steps, int nn, int variant, double* ms_out);
@@ -210,6 +211,9 @@ uint64_t hp_launch_count(hp_ctx* ctx);   /* kernels launched by this context so 
 /* Tuning sweeps: select the tuned-stencil configuration (vector width x CTAs
  * per SM, process-wide); returns the number of configurations, <0 if invalid. */
 int hp_set_stencil_config(int cfg);
+/* Two Jacobi iterations per stencil pass in the device time loop (opt-in);
+ * returns the previous setting.  Default off. */
+int hp_set_temporal_blocking(int on);
 
 /* ---- slab decomposition over several GPUs -----------------
  * The interior planes [1, I-2) of the slowest dimension are split into

@@ -75,6 +75,7 @@ inline LaunchArgs ctx_args(const hp_ctx* c, int reset) {
 int time_loop_begin(hp_ctx* c, const LaunchArgs& a);
 int time_loop_step(hp_ctx* c, int it, const LaunchArgs& a);
 int time_loop_end(hp_ctx* c, int nn, const LaunchArgs& a);
+int time_loop_finish(hp_ctx* c, float* last, const LaunchArgs& a);
 float* time_loop_buffer(hp_ctx* c, int it);   // buffer holding p after `it` steps
 void dd_destroy(hp_ctx* c);                   // decomp.cpp
 // Whole-field host <-> device copies: one contiguous PCIe transfer through the

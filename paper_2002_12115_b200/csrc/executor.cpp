@@ -150,7 +150,9 @@ int hp::time_loop_step(hp_ctx* c, int it, const LaunchArgs& a) {
                                c->sink(), c->stream);
 }
 int hp::time_loop_end(hp_ctx* c, int nn, const LaunchArgs& a) {
-  float* last = time_loop_buffer(c, nn);
+  return time_loop_finish(c, time_loop_buffer(c, nn), a);
+}
+int hp::time_loop_finish(hp_ctx* c, float* last, const LaunchArgs& a) {
   int n = 0, r;
   if ((r = launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a, c->stream)) < 0)
     return -1;
@@ -781,15 +783,17 @@ struct Runner {
   }
 
  public:
+  // the fused device time loop: one- and two-step passes (temporal blocking)
   static int time_loop_fused(hp_ctx* c, int nn, const LaunchArgs& a) {
     int n = 0, r;
     if ((r = time_loop_begin(c, a)) < 0) return -1;
     n += r;
-    for (int it = 0; it < nn; ++it) {
-      if ((r = time_loop_step(c, it, a)) < 0) return -1;
-      n += r;
-    }
-    if ((r = time_loop_end(c, nn, a)) < 0) return -1;
+    float* last = nullptr;
+    if ((r = stencil_iterations(c->dev, c->dev.f[HP_F_P], c->scratch, nn, a, c->sink(),
+                                c->stream, &last, nullptr)) < 0)
+      return -1;
+    n += r;
+    if ((r = time_loop_finish(c, last, a)) < 0) return -1;
     return n + r;
   }
 
@@ -1065,6 +1069,8 @@ extern "C" int hp_jacobi_device(hp_ctx* c, int nn, int variant) {
 
 extern "C" uint64_t hp_launch_count(hp_ctx* c) { return c ? c->launches : 0; }
 
+extern "C" int hp_set_temporal_blocking(int on) { return set_temporal_blocking(on); }
+
 extern "C" int hp_set_stencil_config(int cfg) {
   const int n = set_stencil_config(cfg);
   if (n < 0) {
@@ -1116,12 +1122,23 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
     ok = ok && launch_copy_halo(c->dev, bufs[0], bufs[1], a, c->stream) >= 0;
     is_stencil.push_back(0);
     ok = ok && mark();
-    for (int it = 0; ok && it < nn; ++it) {
-      ok = launch_stencil_rotate(c->dev, bufs[it & 1], bufs[(it + 1) & 1], a, c->sink(),
-                                 c->stream) >= 0 && mark();
+    float* cur = bufs[0];
+    float* oth = bufs[1];
+    int it = 0;
+    while (ok && it < nn) {
+      // one pass at a time (same choice as stencil_iterations), an event after each
+      float* last = nullptr;
+      int passes = 0;
+      const int step = (nn - it >= 2) ? 2 : 1;
+      ok = stencil_iterations(c->dev, cur, oth, step, a, c->sink(), c->stream, &last, &passes) >= 0;
+      ok = ok && mark();   // (a 2-step request may have run as two single passes)
       is_stencil.push_back(1);
+      out->stencil_iters += step;
+      it += step;
+      cur = last;
+      oth = last == bufs[0] ? bufs[1] : bufs[0];
     }
-    float* last = bufs[nn & 1];
+    float* last = cur;
     ok = ok && launch_copy_interior_bounds(c->dev, last, c->dev.f[HP_F_WRK2], a, c->stream) >= 0 && mark();
     is_stencil.push_back(0);
     if (ok && last != c->dev.f[HP_F_P]) {
@@ -1133,6 +1150,7 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
     for (int it = 0; ok && it < nn; ++it) {
       ok = launch_stencil_3d(c->dev, a, c->sink(), c->stream) >= 0 && mark();
       is_stencil.push_back(1);
+      out->stencil_iters += 1;
       ok = ok && launch_copy_3d(c->dev, a, c->stream) >= 0 && mark();
       is_stencil.push_back(0);
     }
@@ -1153,6 +1171,7 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
     cudaEventElapsedTime(&total, ev.front(), ev.back());
     out->total_ms = total;
     out->stencil_ms = out->n_stencil ? st / out->n_stencil : 0.0;
+    out->stencil_iters = out->n_stencil ? out->stencil_iters / out->n_stencil : 0.0;
     out->other_ms = out->n_other ? ot / out->n_other : 0.0;
   }
   for (cudaEvent_t e : ev) cudaEventDestroy(e);

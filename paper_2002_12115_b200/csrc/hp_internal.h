@@ -104,6 +104,14 @@ void destroy_stencil_tma(void* h);
 int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, float* p_out,
                        const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int stages,
                        int sms);
+// two Jacobi iterations per pass (temporal blocking); 0 = not applicable
+int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                       const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms);
+// run iterations [0, nn) p_in -> ... choosing one- or two-step passes; sets
+// *last to the buffer holding p_nn; returns kernels launched or -1
+int stencil_iterations(const DevFields& F, float* buf0, float* buf1, int nn, const LaunchArgs& a,
+                       const GosaSink& g, cudaStream_t s, float** last, int* stencil_launches);
+int set_temporal_blocking(int on);
 
 // ---- host loop bodies (executor.cpp), same arithmetic as the kernels --------
 struct HostFields {

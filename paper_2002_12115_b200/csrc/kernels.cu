@@ -486,6 +486,40 @@ int stencil_grid(int cfg) {
 
 }  // namespace
 
+int g_temporal_blocking = 0;   // two-step passes (stencil_tma.cu): opt-in, see DESIGN.md §5
+
+int set_temporal_blocking(int on) {
+  const int old = g_temporal_blocking;
+  g_temporal_blocking = on ? 1 : 0;
+  return old;
+}
+
+int stencil_iterations(const DevFields& F, float* buf0, float* buf1, int nn, const LaunchArgs& a,
+                       const GosaSink& g, cudaStream_t s, float** last, int* stencil_launches) {
+  float* cur = buf0;
+  float* oth = buf1;
+  int n = 0, it = 0;
+  while (it < nn) {
+    int r = 0;
+    if (g_temporal_blocking && nn - it >= 2) {
+      r = launch_stencil_tb2(F, F.tma, cur, oth, a, g, s, sm_count());
+      if (r > 0) it += 2;
+    }
+    if (r == 0) {
+      r = launch_stencil_rotate(F, cur, oth, a, g, s);
+      it += 1;
+    }
+    if (r < 0) return -1;
+    n += r;
+    if (stencil_launches) ++*stencil_launches;
+    float* t = cur;
+    cur = oth;
+    oth = t;
+  }
+  *last = cur;
+  return n;
+}
+
 int set_stencil_config(int cfg) {
   if (cfg < 0 || cfg >= kNumStencilCfgs) return -1;
   g_stencil_cfg = cfg;

@@ -24,13 +24,17 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hp_internal.h"
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace hp {
 namespace {
+using namespace tma;
 
 constexpr int TJ = 8;                 // rows per tile = consumer warps
 constexpr int TK = 128;               // k per tile (32 lanes x float4)
@@ -50,52 +54,6 @@ struct __align__(64) StencilMaps {
   CUtensorMap coef[NCOEF];
   CUtensorMap pin;
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Bounded wait: a pipeline bug must abort the kernel (trap -> launch error),
-// never hang the GPU.  2^26 polls (each try_wait suspends up to a
-// hardware-defined interval) is seconds, far beyond any legitimate wait.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (uint32_t n = 0; n < (1u << 26); ++n) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-  }
-  asm volatile("trap;");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
 
 struct Row {            // one p row quad of a lane + its k-1 / k+4 neighbours
   float4 v;
@@ -276,46 +234,274 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
   gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
 }
 
-// ------------------------------------------------------------------ host side
+// ================================================================ two-step kernel
+//
+// k_stencil_tb2: two Jacobi iterations per pass (temporal blocking).  Output
+// tile = TJ2 rows x 128 k; step 1 computes p1 = S(p0) on the tile extended by
+// one row / column on each side (R1 = TJ2+2 rows, 130 columns) so that step 2
+// can compute p2 = S(p1) on the tile one plane behind.  The 12 coefficient
+// arrays are read from HBM once for both iterations: 56 B per point per TWO
+// iterations (vs 2 x 56 for two single-step passes).
+//
+//   producer warp: p0 plane tiles (136k x (R1+2)j) into a 4-slot ring, extended
+//     coefficient tiles (136k x R1 j, 12 arrays) into a 3-slot ring.
+//   consumer warp w (0..R1-1) <-> row j0-1+w:
+//     step 1 (plane m): register queue of p0 rows, lanes = k-quads, lane 0 / 31
+//       also the extra columns k0-1 / k0+128 (scalars from the p0 ring);
+//       non-interior points copy p0 (boundaries are fixed).  p1 -> smem (2 slots).
+//     named barrier among the consumer warps (p1(m) complete)
+//     step 2 (plane m-1, warps 1..TJ2): register queue of p1 rows; coefficients
+//       of plane m-1 are still resident in the coefficient ring.
+// Every product/sum rounds exactly like the single-step kernel: p2 is
+// bit-identical to two single steps; gosa (fp64) is that of the second step.
+constexpr int TJ2 = 6;                 // output rows per tile
+constexpr int R1 = TJ2 + 2;            // step-1 rows = consumer warps
+constexpr int kThreads2 = (R1 + 1) * 32;
+constexpr uint32_t kP0Bytes = PW * (R1 + 2) * 4;           // 5440
+constexpr uint32_t kP0Slot = (kP0Bytes + 127) / 128 * 128;
+constexpr uint32_t kCExtBytes = PW * R1 * 4;               // 4352 per array
+constexpr uint32_t kCSlot = NCOEF * kCExtBytes;            // 52224
+constexpr uint32_t kP1Slot = PW * R1 * 4;                  // 4352
+constexpr int SP = 4, SC = 3, SQ = 2;                      // p0 / coef / p1 ring slots
+constexpr uint32_t kTb2Smem = SP * kP0Slot + SC * kCSlot + SQ * kP1Slot;
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+struct __align__(64) Tb2Maps {
+  CUtensorMap coef[NCOEF];   // box 136 x R1
+  CUtensorMap pin;           // box 136 x (R1+2)
+};
 
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-    else
-      cudaGetLastError();
+// one step of the stencil at element x of lane quads (rows: m* plane i, l* i-1, n* i+1)
+__device__ __forceinline__ float ss_point(const float* q, const Row& lm, const Row& l0,
+                                          const Row& lp, const Row& mm, const Row& m0,
+                                          const Row& mp, const Row& nm, const Row& n0,
+                                          const Row& np, int x) {
+  float s0 = fmul(q[CA0], el(n0.v, x));
+  s0 = fadd(s0, fmul(q[CA1], el(mp.v, x)));
+  s0 = fadd(s0, fmul(q[CA2], kp1(m0, x)));
+  s0 = fadd(s0, fmul(q[CB0], fadd(fsub(fsub(el(np.v, x), el(nm.v, x)), el(lp.v, x)), el(lm.v, x))));
+  s0 = fadd(s0, fmul(q[CB1], fadd(fsub(fsub(kp1(mp, x), kp1(mm, x)), km1(mp, x)), km1(mm, x))));
+  s0 = fadd(s0, fmul(q[CB2], fadd(fsub(fsub(kp1(n0, x), kp1(l0, x)), km1(n0, x)), km1(l0, x))));
+  s0 = fadd(s0, fmul(q[CC0], el(l0.v, x)));
+  s0 = fadd(s0, fmul(q[CC1], el(mm.v, x)));
+  s0 = fadd(s0, fmul(q[CC2], km1(m0, x)));
+  s0 = fadd(s0, q[CW1]);
+  return fmul(fsub(fmul(s0, q[CA3]), el(m0.v, x)), q[CBN]);
+}
+
+// the same on scalars read from shared-memory tiles: P(plane, drow, dcol)
+template <class PF>
+__device__ __forceinline__ float ss_scalar(const float* q, PF P) {
+  float s0 = fmul(q[CA0], P(1, 0, 0));
+  s0 = fadd(s0, fmul(q[CA1], P(0, 1, 0)));
+  s0 = fadd(s0, fmul(q[CA2], P(0, 0, 1)));
+  s0 = fadd(s0, fmul(q[CB0], fadd(fsub(fsub(P(1, 1, 0), P(1, -1, 0)), P(-1, 1, 0)), P(-1, -1, 0))));
+  s0 = fadd(s0, fmul(q[CB1], fadd(fsub(fsub(P(0, 1, 1), P(0, -1, 1)), P(0, 1, -1)), P(0, -1, -1))));
+  s0 = fadd(s0, fmul(q[CB2], fadd(fsub(fsub(P(1, 0, 1), P(-1, 0, 1)), P(1, 0, -1)), P(-1, 0, -1))));
+  s0 = fadd(s0, fmul(q[CC0], P(-1, 0, 0)));
+  s0 = fadd(s0, fmul(q[CC1], P(0, -1, 0)));
+  s0 = fadd(s0, fmul(q[CC2], P(0, 0, -1)));
+  s0 = fadd(s0, q[CW1]);
+  return fmul(fsub(fmul(s0, q[CA3]), P(0, 0, 0)), q[CBN]);
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads2, 1)
+k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
+              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles,
+              float omega, GosaSink g, int reset) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  unsigned char* p0ring = smem;
+  unsigned char* cring = p0ring + SP * kP0Slot;
+  float* p1ring = reinterpret_cast<float*>(cring + SC * kCSlot);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTb2Smem);
+  uint64_t* pfull = bars;
+  uint64_t* pempty = pfull + SP;
+  uint64_t* cfull = pempty + SP;
+  uint64_t* cempty = cfull + SC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ni = i_hi - i_lo;
+  const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
+  const long long U = (long long)ktiles * jtiles * ni;
+  Walker walk{U * blockIdx.x / gridDim.x, U * (blockIdx.x + 1) / gridDim.x, ni, ktiles};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], R1); }
+    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  return fn;
+  __syncthreads();
+  double acc = 0.0;
+  if (warp == R1) {
+    // ------------------------------------------------------------- producer
+    if (lane == 0) {
+      uint32_t sp = 0, sc = 0;
+      Unit s{0, 0, 0, 0};
+      auto load_p0 = [&](const Unit& u, int plane) {
+        const int slot = sp % SP;
+        if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
+        mbar_expect_tx(&pfull[slot], kP0Bytes);
+        tma_load_3d(p0ring + slot * kP0Slot, &maps.pin, &pfull[slot], u.kt * TK - 4,
+                    j_lo + u.jt * TJ2 - 2, plane);
+        ++sp;
+      };
+      auto load_c = [&](const Unit& u, int plane) {
+        const int slot = sc % SC;
+        if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
+        mbar_expect_tx(&cfull[slot], NCOEF * kCExtBytes);
+        for (int m = 0; m < NCOEF; ++m)
+          tma_load_3d(cring + slot * kCSlot + m * kCExtBytes, &maps.coef[m], &cfull[slot],
+                      u.kt * TK - 4, j_lo + u.jt * TJ2 - 1, plane);
+        ++sc;
+      };
+      while (walk.next(s)) {
+        const int ia = i_lo + s.ia, ib = i_lo + s.ib;
+        load_p0(s, ia - 2);
+        load_p0(s, ia - 1);
+        for (int m = ia - 1; m <= ib; ++m) {
+          load_p0(s, m + 1);
+          load_c(s, m);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    uint32_t sp = 0, sc = 0;   // consumed counts of the two rings
+    uint32_t it = 0;           // p1 slot counter
+    Unit s;
+    const int imax1 = i_hi;    // planes [i_lo, i_hi) are the global interior
+    while (walk.next(s)) {
+      const int ia = i_lo + s.ia, ib = i_lo + s.ib;
+      const int j1 = j_lo + s.jt * TJ2 - 1 + warp;      // this warp's step-1 row
+      const int k0 = s.kt * TK;
+      const int kb = k0 + lane * 4;
+      const bool row_in = j1 >= j_lo && j1 < j_hi;
+      bool in1[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) in1[x] = row_in && kb + x >= k_lo && kb + x < k_hi;
+      const bool out_row = warp >= 1 && warp <= TJ2 && row_in;   // step-2 output row
+      // p0 queue: planes m-1 (a*), m (b*); p0 slot of plane q = sequence sp0 + (q - (ia-2))
+      const uint32_t sp0 = sp;
+      Row am, a0, ap, bm, b0, bp;
+      for (int w = 0; w < 2; ++w) {
+        const int slot = sp % SP;
+        mbar_wait(&pfull[slot], (sp / SP) & 1);
+        const float* pt = reinterpret_cast<const float*>(p0ring + slot * kP0Slot);
+        const Row x0 = load_row(pt, warp, lane), x1 = load_row(pt, warp + 1, lane),
+                  x2 = load_row(pt, warp + 2, lane);
+        if (w == 0) { am = x0; a0 = x1; ap = x2; } else { bm = x0; b0 = x1; bp = x2; }
+        ++sp;
+      }
+      // first p0 plane (ia-2) is only needed by step1(ia-1)'s scalars: released in-loop
+      Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
+      for (int m = ia - 1; m <= ib; ++m) {
+        const int pslot = sp % SP;
+        mbar_wait(&pfull[pslot], (sp / SP) & 1);
+        const float* pt = reinterpret_cast<const float*>(p0ring + pslot * kP0Slot);
+        const Row cm = load_row(pt, warp, lane), c0 = load_row(pt, warp + 1, lane),
+                  cp = load_row(pt, warp + 2, lane);
+        ++sp;
+        const int cslot = sc % SC;
+        mbar_wait(&cfull[cslot], (sc / SC) & 1);
+        ++sc;
+        const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot);
+        // ---- step 1 at plane m, row j1 -> p1 slot
+        float* q1 = p1ring + (it % SQ) * (PW * R1);
+        const bool plane_in = m >= i_lo && m < imax1;
+        float r[4];
+        float qv[4][NCOEF];
+#pragma unroll
+        for (int c = 0; c < NCOEF; ++c) {
+          const float4 t = *reinterpret_cast<const float4*>(ct + c * (PW * R1) + warp * PW + 4 + lane * 4);
+          qv[0][c] = t.x; qv[1][c] = t.y; qv[2][c] = t.z; qv[3][c] = t.w;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          r[x] = (plane_in && in1[x]) ? fadd(el(b0.v, x), fmul(omega, ss_point(qv[x], am, a0, ap,
+                                                                                  bm, b0, bp, cm,
+                                                                                  c0, cp, x)))
+                                      : el(b0.v, x);
+        *reinterpret_cast<float4*>(q1 + warp * PW + 4 + lane * 4) = make_float4(r[0], r[1], r[2], r[3]);
+        if (lane == 0 || lane == 31) {
+          // extra column k0-1 (lane 0) / k0+128 (lane 31), scalars from the p0 ring
+          const int col = lane == 0 ? 3 : 4 + TK;
+          const int k = k0 - 4 + col;
+          const float* pl[3];
+          for (int d = 0; d < 3; ++d)
+            pl[d] = reinterpret_cast<const float*>(p0ring + ((sp0 + (m - (ia - 2)) - 1 + d) % SP) * kP0Slot);
+          auto P = [&](int di, int dj, int dk) { return pl[di + 1][(warp + 1 + dj) * PW + col + dk]; };
+          float v = P(0, 0, 0);
+          if (plane_in && row_in && k >= k_lo && k < k_hi) {
+            float qs[NCOEF];
+            for (int c = 0; c < NCOEF; ++c) qs[c] = ct[c * (PW * R1) + warp * PW + col];
+            v = fadd(v, fmul(omega, ss_scalar(qs, P)));
+          }
+          q1[warp * PW + col] = v;
+        }
+        // p0 plane m-1 is no longer needed (scalars of step1(m) were its last use)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[(sp0 + (m - (ia - 2)) - 1) % SP]);
+        named_bar(1, R1 * 32);
+        // ---- p1(m) rows into the queue; step 2 at plane m-1
+        const Row nm = load_row(q1, warp > 0 ? warp - 1 : 0, lane),
+                  n0 = load_row(q1, warp, lane),
+                  np = load_row(q1, warp < R1 - 1 ? warp + 1 : R1 - 1, lane);
+        if (m >= ia + 1 && out_row) {
+          const int pc = (sc - 2) % SC;   // coefficient slot of plane m-1
+          const float* cq = reinterpret_cast<const float*>(cring + pc * kCSlot);
+          float q2[4][NCOEF];
+#pragma unroll
+          for (int c = 0; c < NCOEF; ++c) {
+            const float4 t = *reinterpret_cast<const float4*>(cq + c * (PW * R1) + warp * PW + 4 + lane * 4);
+            q2[0][c] = t.x; q2[1][c] = t.y; q2[2][c] = t.z; q2[3][c] = t.w;
+          }
+          float w2[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const float ss = ss_point(q2[x], ym, y0, yp, zm, z0, zp, nm, n0, np, x);
+            w2[x] = fadd(el(z0.v, x), fmul(omega, ss));
+            if (in1[x]) acc += (double)fmul(ss, ss);
+          }
+          float* o = out + F.at(m - 1, j1, kb);
+          if (in1[0] && in1[1] && in1[2] && in1[3]) {
+            *reinterpret_cast<float4*>(o) = make_float4(w2[0], w2[1], w2[2], w2[3]);
+          } else {
+            for (int x = 0; x < 4; ++x)
+              if (in1[x]) o[x] = w2[x];
+          }
+        }
+        // release coefficient stages: plane m-1 after its step 2, plane ia-1 / ib after step 1
+        __syncwarp();
+        if (lane == 0) {
+          if (m >= ia + 1) mbar_arrive(&cempty[(sc - 2) % SC]);
+          if (m == ia - 1 || m == ib) mbar_arrive(&cempty[(sc - 1) % SC]);
+        }
+        ym = zm; y0 = z0; yp = zp;
+        zm = nm; z0 = n0; zp = np;
+        am = bm; a0 = b0; ap = bp;
+        bm = cm; b0 = c0; bp = cp;
+        ++it;
+      }
+      // release the p0 planes ib and ib+1 (and nothing else remains)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&pempty[(sp - 2) % SP]);
+        mbar_arrive(&pempty[(sp - 1) % SP]);
+      }
+    }
+  }
+  gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
 }
 
-bool encode(CUtensorMap* m, const DevFields& F, const float* base, uint32_t box_k, uint32_t box_j) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)F.P, (cuuint64_t)F.J, (cuuint64_t)F.I};
-  const cuuint64_t strides[2] = {(cuuint64_t)F.P * 4, (cuuint64_t)F.plane() * 4};
-  const cuuint32_t box[3] = {box_k, box_j, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
+// ------------------------------------------------------------------ host side
 
 struct TmaState {
   StencilMaps base;          // coefficient maps + p map
   CUtensorMap scratch_map;   // p map of the rotation buffer
+  Tb2Maps tb2;               // two-step kernel: extended coefficient boxes + p map
+  CUtensorMap tb2_scratch;
   const float* p;
   const float* scratch;
 };
@@ -324,16 +510,33 @@ struct TmaState {
 
 // Build the tensor maps of one context (fields + rotation scratch); nullptr if
 // the driver cannot encode them (the caller then uses k_stencil_3d).
+// HIMENO_TMA_PROMO="a,b,c,d": L2 promotion codes (0 none, 1 64B, 2 128B, 3 256B)
+// of the single-step coefficient / p maps and the two-step coefficient / p maps.
+static void promo_codes(int* c) {
+  c[0] = 2; c[1] = 2; c[2] = 0; c[3] = 0;
+  if (const char* e = getenv("HIMENO_TMA_PROMO"))
+    sscanf(e, "%d,%d,%d,%d", &c[0], &c[1], &c[2], &c[3]);
+}
+
 void* create_stencil_tma(const DevFields& F, const float* scratch) {
   TmaState* t = new TmaState;
+  int pc[4];
+  promo_codes(pc);
   bool ok = true;
   for (int m = 0; m < NCOEF; ++m) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ);
+    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ, pc[0]);
   }
-  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH);
-  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH);
+  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1]);
+  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1]);
+  for (int m = 0; m < NCOEF; ++m) {
+    static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
+                                      HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
+    ok = ok && encode(&t->tb2.coef[m], F, F.f[fields[m]], PW, R1, pc[2]);
+  }
+  ok = ok && encode(&t->tb2.pin, F, F.f[HP_F_P], PW, R1 + 2, pc[3]);
+  ok = ok && encode(&t->tb2_scratch, F, scratch, PW, R1 + 2, pc[3]);
   t->p = F.f[HP_F_P];
   t->scratch = scratch;
   if (!ok) {
@@ -381,6 +584,38 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
     case 4: launch(k_stencil_tma<4>); break;
     default: return 0;
   }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not
+// applicable: caller runs two single steps), or -1 on launch error.
+int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                       const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+  const TmaState* t = static_cast<const TmaState*>(h);
+  if (!t || (p_in != t->p && p_in != t->scratch)) return 0;
+  const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
+            k_hi = a.kmax - 1;
+  // full grid only (a slab's halo would need two planes per exchange)
+  if (a.i_off != 0 || i_lo != 1 || i_hi != a.imax - 1) return 0;
+  if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
+  Tb2Maps maps = t->tb2;
+  if (p_in == t->scratch) maps.pin = t->tb2_scratch;
+  const int ktiles = (k_hi + TK - 1) / TK;
+  const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
+  const long long units = (long long)ktiles * jtiles * (i_hi - i_lo);
+  long long grid = sms;
+  if (grid > units) grid = units;
+  if (grid > g.capacity) return -1;
+  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC) * sizeof(uint64_t);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_stencil_tb2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  k_stencil_tb2<<<(int)grid, kThreads2, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo,
+                                                   k_hi, ktiles, a.omega, g, a.gosa_reset);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -77,7 +77,7 @@ class Result(C.Structure):
 
 class KernelTimes(C.Structure):
     _fields_ = [("total_ms", C.c_double), ("stencil_ms", C.c_double), ("other_ms", C.c_double),
-                ("n_stencil", C.c_int32), ("n_other", C.c_int32)]
+                ("stencil_iters", C.c_double), ("n_stencil", C.c_int32), ("n_other", C.c_int32)]
 
 
 # exported symbols: name -> (restype, argtypes); tests check every one exists
@@ -103,6 +103,7 @@ SIGNATURES = {
     "hp_time_jacobi": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(KernelTimes)]),
     "hp_launch_count": (C.c_uint64, [_CtxP]),
     "hp_set_stencil_config": (C.c_int, [C.c_int]),
+    "hp_set_temporal_blocking": (C.c_int, [C.c_int]),
     "hp_slab_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32)]),
     "hp_create_slab": (C.c_int, [C.c_int, C.POINTER(Grid), C.c_int, C.c_int, C.POINTER(_CtxP)]),

@@ -172,3 +172,32 @@ def test_every_stencil_config_bit_exact(gpu, name, nn):
                     assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], (cfg, variant)
     finally:
         lib.hp_set_stencil_config(7)
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("name,nn", [("XS", 1), ("XS", 4), ("XS", 5), ("M", 2), ("M", 3),
+                                      ("custom", 4), ("ragged", 3)])
+def test_temporal_blocking_bit_exact(gpu, tb, name, nn):
+    """Two-step passes (temporal blocking) reproduce nn single iterations exactly."""
+    if name == "custom":
+        sz = himeno.custom_size(37, 21, 70)
+    elif name == "ragged":
+        sz = himeno.custom_size(20, 29, 300)
+    else:
+        sz = himeno.size(name)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            p, w, g = ctx.read_field("p", 1), ctx.read_field("wrk2", 1), ctx.read_gosa(1)
+            kt = ctx.time_jacobi(nn, 1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert np.array_equal(w, ref["fields"]["wrk2"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+    if tb and nn >= 2:
+        assert kt.stencil_iters > 1.0

@@ -168,6 +168,10 @@ def run_reference(args, world, rank):
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if not args.no_ga:
+        from oracle import ref_ga
+        line["ga"] = ref_ga.ga_throughput(args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
+                                          args.ga_seed)
     print(json.dumps(line), flush=True)
     return 0
 

@@ -6,8 +6,9 @@
 Workload (BASELINE.json configs; north_star's headline grid): Himeno L
 (257 x 257 x 513, fp32), the best gene pattern's jacobi(nn): the device-resident
 time loop (gene 6; fused stencil with p/wrk2 rotation).  One *step* =
-one jacobi(nn) call, nn = 10 iterations.  Inputs (1.9 GB) exceed the 126 MB L2,
-so no flush is needed between steps.  GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
+one jacobi(nn) call, nn = 100 iterations (N = 100).
+Inputs (1.9 GB) exceed the 126 MB L2, so no flush is needed between steps.
+GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
 
 * value      device-resident: K steps between CUDA events on the library's
              stream, barrier + synchronize on both sides, max over ranks.
@@ -355,11 +356,11 @@ def run_ours(args, world, rank, local):
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--size", default="L")
-    ap.add_argument("--nn", type=int, default=10)
+    ap.add_argument("--nn", type=int, default=100)
     ap.add_argument("--variant", type=int, default=1, choices=[0, 1])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-ga", action="store_true")

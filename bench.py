@@ -177,10 +177,11 @@ def run_reference(args, world, rank):
     return 0
 
 
-def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, seed: int) -> dict:
+def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, seed: int,
+                  workers: int = 1) -> dict:
     from paper_2002_12115_b200 import ga
     from paper_2002_12115_b200.evaluator import B200Evaluator
-    with B200Evaluator(size_name, nn=nn, devices=[device]) as ev:
+    with B200Evaluator(size_name, nn=nn, devices=[device], workers_per_device=workers) as ev:
         ev.measure((0,) * ev.gene_length)                  # context + first-touch warm-up
         t0 = time.perf_counter()
         res = ga.run_ga(ga.GAConfig(population=pop, generations=gens, rng_seed=seed),
@@ -188,7 +189,8 @@ def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, see
         el = time.perf_counter() - t0
         ok = sum(1 for r in res.records for i in r.individuals if i.eval_source == "fresh")
     return {"size": size_name, "nn": nn, "population": pop, "generations": gens, "seed": seed,
-            "wall_s": el, "fresh_evals": res.evaluations, "valid_fresh": ok,
+            "workers_per_gpu": workers, "wall_s": el, "fresh_evals": res.evaluations,
+            "valid_fresh": ok,
             "evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
             "best_genome": ga.genome_str(res.best.genome), "best_time_s": res.best.time_s}
 
@@ -324,7 +326,7 @@ def run_ours(args, world, rank, local):
         extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
     if rank == 0 and not args.no_ga:
         extra["ga"] = ga_throughput(local, args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
-                                    args.ga_seed)
+                                    args.ga_seed, args.ga_workers)
     if slab is not None:
         slab.close()
     else:
@@ -371,6 +373,8 @@ def main(argv=None) -> int:
     ap.add_argument("--ga-pop", type=int, default=20)
     ap.add_argument("--ga-gens", type=int, default=10)
     ap.add_argument("--ga-seed", type=int, default=0)
+    ap.add_argument("--ga-workers", type=int, default=4,
+                    help="concurrent evaluations per GPU (own context each)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

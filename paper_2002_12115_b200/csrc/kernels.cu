@@ -488,9 +488,10 @@ int stencil_grid(int cfg) {
 
 int g_temporal_blocking = 0;   // two-step passes (stencil_tma.cu): opt-in, see DESIGN.md §5
 
+// on < 0: query only
 int set_temporal_blocking(int on) {
   const int old = g_temporal_blocking;
-  g_temporal_blocking = on ? 1 : 0;
+  if (on >= 0) g_temporal_blocking = on ? 1 : 0;
   return old;
 }
 

@@ -8,9 +8,10 @@ Plugin contract (acctuner/ga.py:222-230, evaluators.py:108-128, 168-188):
   ``MeasuredTime.failed`` (penalty, GA continues), timeouts as
   ``MeasuredTime.timeout``; environment problems *raise*
   ``EvaluatorUnavailable`` (``NativeUnavailable`` / ``DeviceError``).
-* ``max_concurrency`` -- number of B200s: ``run_ga`` measures up to that many
-  fresh genomes at once (one per GPU, population sharding with no
-  collectives).  Each call leases a device context.
+* ``max_concurrency`` -- number of worker slots (B200s x ``workers_per_device``):
+  ``run_ga`` measures up to that many fresh genomes at once (population
+  sharding with no collectives).  Each call leases a slot,
+  which owns its own device context.
 * ``deterministic = False`` -- times are measured.
 
 What replaces compile+run: ``Planner.plan(genome)`` (plan.py, same plan as the
@@ -76,7 +77,8 @@ class B200Evaluator:
                  eligible_ids=None, kinds=None, transfer_mode: str = "batched",
                  nested_policy: str = "reject", coherence_guard: bool = True,
                  fused_time_loop: bool = True, fresh_process: bool = True,
-                 poison_device: bool = False, timeout_s: float = 180.0):
+                 poison_device: bool = False, timeout_s: float = 180.0,
+                 workers_per_device: int = 1):
         if transfer_mode not in TRANSFER_MODES:
             raise ConfigError(f"transfer_mode must be one of {TRANSFER_MODES}")
         if nested_policy not in NESTED_POLICIES:
@@ -102,7 +104,9 @@ class B200Evaluator:
             devices = [0]
         elif devices == "all":
             devices = list(range(N.device_count()))
-        self.devices = list(devices)
+        # one worker slot per entry; a device may appear several times (several
+        # concurrent evaluations on one GPU, each with its own context)
+        self.devices = list(devices) * max(1, int(workers_per_device))
         if not self.devices:
             raise EvaluatorUnavailable("no CUDA devices to evaluate on")
         self.max_concurrency = len(self.devices)
@@ -110,11 +114,12 @@ class B200Evaluator:
         self._contexts: dict = {}
         self._ctx_lock = threading.Lock()
         self._free: "queue.Queue[int]" = queue.Queue()
-        for d in self.devices:
-            self._free.put(d)
+        for slot in range(len(self.devices)):
+            self._free.put(slot)
         self._lowered: dict = {}
         self._low_lock = threading.Lock()
         self.stats: dict = {}          # genome -> native result stats of its last run
+        self._last_slot = 0
         self.evaluations = 0
 
     # -- construction from the reference pipeline objects ----------------------
@@ -142,11 +147,7 @@ class B200Evaluator:
             low = self._lowered.get(genome)
         if low is None:
             self.planner.gene_map(genome)   # length check -> GenomeLengthMismatch
-            plan = None
-            try:
-                plan = self.plan(genome)
-            except Exception:
-                raise
+            plan = self.plan(genome)
             low = lower(genome, self.eligible_ids, self.kinds, self.loops, self.refs, plan,
                         self.nn, self.flags, self.timeout_s, self.nested_policy)
             with self._low_lock:
@@ -154,25 +155,26 @@ class B200Evaluator:
         return low
 
     # -- device contexts ---------------------------------------------------------------
-    def _context(self, device: int) -> N.Context:
+    def _context(self, slot: int) -> N.Context:
         with self._ctx_lock:
-            ctx = self._contexts.get(device)
+            ctx = self._contexts.get(slot)
             if ctx is None:
                 sz = self.size
-                ctx = N.Context(device, sz.I, sz.J, sz.K)
+                ctx = N.Context(self.devices[slot], sz.I, sz.J, sz.K)
                 ctx.set_samples(sz.sample_points())
-                self._contexts[device] = ctx
+                self._contexts[slot] = ctx
             return ctx
 
     def _execute(self, genome):
         low = self.lowered(genome)
         if low.failure is not None:
             return low, None
-        device = self._free.get()
+        slot = self._free.get()
         try:
-            res = self._context(device).run(low.schedule)
+            res = self._context(slot).run(low.schedule)
+            self._last_slot = slot
         finally:
-            self._free.put(device)
+            self._free.put(slot)
         return low, res
 
     # -- plugin API ----------------------------------------------------------------------
@@ -208,9 +210,10 @@ class B200Evaluator:
         lines += [f"{float(v):.9e}" for v in res.samples[:res.n_samples]]
         return "\n".join(lines) + "\n"
 
-    def read_field(self, name: str, device: Optional[int] = None, side: int = 0):
-        """Host (side 0) or device (1) copy of a field after the last run on `device`."""
-        return self._context(self.devices[0] if device is None else device).read_field(name, side)
+    def read_field(self, name: str, slot: Optional[int] = None, side: int = 0):
+        """Host (side 0) or device (1) copy of a field after the last run in a worker slot
+        (default: the slot of the most recent run)."""
+        return self._context(self._last_slot if slot is None else slot).read_field(name, side)
 
     def close(self) -> None:
         with self._ctx_lock:

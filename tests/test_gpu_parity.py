@@ -201,3 +201,20 @@ def test_temporal_blocking_bit_exact(gpu, tb, name, nn):
     assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
     if tb and nn >= 2:
         assert kt.stencil_iters > 1.0
+
+
+def test_concurrent_workers_share_a_device(gpu):
+    """Population sharding with several worker slots (own contexts) on one GPU."""
+    from concurrent.futures import ThreadPoolExecutor
+    ref = oracle_result("XS", 3)
+    with B200Evaluator("XS", nn=3, workers_per_device=3) as ev:
+        assert ev.max_concurrency == 3
+        genomes = valid_genomes(ev.loops, ev.eligible_ids)[::23]
+        with ThreadPoolExecutor(max_workers=3) as pool:
+            results = list(pool.map(ev.measure, genomes))
+        assert all(m.seconds for m in results)
+        for g in genomes:
+            st = ev.stats[g]
+            assert abs(st["gosa"] - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], g
+            assert st["n_stale_reads"] == 0
+        assert len(ev._contexts) == 3

@@ -47,6 +47,7 @@ struct hp_ctx {
     g.slot = reinterpret_cast<double*>(dscal + HP_V_GOSA * hp::SLOT_BYTES);
     g.partials = partials;
     g.ticket = ticket;
+    g.work = ticket + 1;
     g.capacity = capacity;
     return g;
   }

@@ -258,9 +258,10 @@ int hp::create_ctx(int device, int I, int J, int K, hp_ctx** out) {
   c->capacity = gosa_capacity_needed(c->dev);
   if ((e = cudaMalloc(&c->partials, (size_t)c->capacity * sizeof(double))) != cudaSuccess)
     return fail(cuda_fail(e, "cudaMalloc(partials)"));
-  if ((e = cudaMalloc(&c->ticket, sizeof(unsigned int))) != cudaSuccess)
+  // [0]: last-block ticket of the gosa reduction, [1]: work-queue counter
+  if ((e = cudaMalloc(&c->ticket, 2 * sizeof(unsigned int))) != cudaSuccess)
     return fail(cuda_fail(e, "cudaMalloc(ticket)"));
-  cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream);
+  cudaMemsetAsync(c->ticket, 0, 2 * sizeof(unsigned int), c->stream);
   cudaMemsetAsync(c->dscal, 0, HP_NVARS * SLOT_BYTES, c->stream);
   cudaMemsetAsync(c->slab, 0, slab_elems * sizeof(float), c->stream);
   cudaEventCreate(&c->ev0);

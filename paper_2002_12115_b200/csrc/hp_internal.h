@@ -45,6 +45,7 @@ struct GosaSink {
   double* partials;
   unsigned int* ticket;
   int capacity;                         // number of partial slots
+  unsigned int* work;                   // dynamic work-queue counter (TMA kernels)
 };
 
 enum Nest { NEST_INIT0 = 0, NEST_INIT1 = 1, NEST_STENCIL = 2, NEST_COPY = 3 };

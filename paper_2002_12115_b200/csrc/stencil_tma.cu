@@ -46,6 +46,16 @@ constexpr uint32_t kPBytes = PW * PH * 4;                    // 5440
 constexpr uint32_t kPSlot = (kPBytes + 127) / 128 * 128;     // 5504
 constexpr uint32_t kCoefBytes = TK * TJ * 4;                 // 4096
 constexpr uint32_t kStageBytes = kPSlot + NCOEF * kCoefBytes;
+// planes per work unit (HIMENO_CHUNK overrides for sweeps)
+static int chunk_planes() {
+  static int c = 0;
+  if (!c) {
+    const char* e = getenv("HIMENO_CHUNK");
+    c = e ? atoi(e) : 32;
+    if (c < 1) c = 32;
+  }
+  return c;
+}
 
 // coefficient slots in smem order (fields a0..a3 b0..b2 c0..c2 wrk1 bnd)
 enum { CA0 = 0, CA1, CA2, CA3, CB0, CB1, CB2, CC0, CC1, CC2, CW1, CBN };
@@ -82,43 +92,45 @@ struct Unit {           // one contiguous run of planes of one tile
   int kt, jt, ia, ib;
 };
 
-// the CTA's segments, identical for producer and consumers
-struct Walker {
-  long long u, u_end;
-  int ni, ktiles;
-  __device__ bool next(Unit& s) {
-    if (u >= u_end) return false;
-    const int t = (int)(u / ni);
-    s.ia = (int)(u % ni);
-    s.ib = (int)min((long long)ni, (long long)s.ia + (u_end - u));
-    u += s.ib - s.ia;
+// Work units = (plane chunk, tile) in chunk-major order, handed out by the
+// device-wide queue (tma.cuh): CTAs that are resident together stream
+// neighbouring tiles over the same planes at the same time, so the halo rows a
+// tile shares with its neighbours are served from L2.
+struct Units {
+  int ni, ktiles, tiles, len;
+  uint32_t count;
+  __device__ void decode(uint32_t u, Unit& s) const {
+    const int t = (int)(u % (uint32_t)tiles), c = (int)(u / (uint32_t)tiles);
     s.kt = t % ktiles;
     s.jt = t / ktiles;
-    return true;
+    s.ia = c * len;
+    s.ib = min(ni, s.ia + len);
   }
 };
 
 template <int S>
 __global__ void __launch_bounds__(kThreads, 1)
 k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __restrict__ out,
-              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles,
+              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
               float omega, GosaSink g, int reset) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // TMA destinations are 128-byte aligned regardless of static smem placement
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
   uint64_t* empty = full + S;
+  UnitRing* ring = reinterpret_cast<UnitRing*>(empty + S);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
-  const long long U = (long long)ktiles * jtiles * ni;
-  Walker walk{U * blockIdx.x / gridDim.x, U * (blockIdx.x + 1) / gridDim.x, ni, ktiles};
+  Units units{ni, ktiles, ktiles * jtiles, chunk,
+              (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], TJ);
     }
+    unit_ring_init(ring, TJ);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -144,7 +156,10 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
                         j_lo + s.jt * TJ, plane_c);
         ++seq;
       };
-      while (walk.next(s)) {
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t u = unit_publish(ring, n, g.work, units.count);
+        if (u == kNoUnit) break;
+        units.decode(u, s);
         const int i0 = i_lo + s.ia, i1 = i_lo + s.ib;
         issue(s, i0 - 1, -1);
         issue(s, i0, -1);
@@ -156,7 +171,10 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
     uint32_t seq = 0;
     Unit s;
     const size_t P = F.P, L = F.plane();
-    while (walk.next(s)) {
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t u = unit_take(ring, n, lane);
+      if (u == kNoUnit) break;
+      units.decode(u, s);
       const int j = j_lo + s.jt * TJ + warp;
       const bool row_ok = j < j_hi;
       const int kb = s.kt * TK + lane * 4;
@@ -310,7 +328,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 __global__ void __launch_bounds__(kThreads2, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
-              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles,
+              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
               float omega, GosaSink g, int reset) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -322,14 +340,16 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   uint64_t* pempty = pfull + SP;
   uint64_t* cfull = pempty + SP;
   uint64_t* cempty = cfull + SC;
+  UnitRing* ring = reinterpret_cast<UnitRing*>(cempty + SC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const long long U = (long long)ktiles * jtiles * ni;
-  Walker walk{U * blockIdx.x / gridDim.x, U * (blockIdx.x + 1) / gridDim.x, ni, ktiles};
+  Units units{ni, ktiles, ktiles * jtiles, chunk,
+              (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], R1); }
     for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1); }
+    unit_ring_init(ring, R1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -356,7 +376,10 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
                       u.kt * TK - 4, j_lo + u.jt * TJ2 - 1, plane);
         ++sc;
       };
-      while (walk.next(s)) {
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t u = unit_publish(ring, n, g.work, units.count);
+        if (u == kNoUnit) break;
+        units.decode(u, s);
         const int ia = i_lo + s.ia, ib = i_lo + s.ib;
         load_p0(s, ia - 2);
         load_p0(s, ia - 1);
@@ -372,7 +395,10 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
     uint32_t it = 0;           // p1 slot counter
     Unit s;
     const int imax1 = i_hi;    // planes [i_lo, i_hi) are the global interior
-    while (walk.next(s)) {
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t u = unit_take(ring, n, lane);
+      if (u == kNoUnit) break;
+      units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int j1 = j_lo + s.jt * TJ2 - 1 + warp;      // this warp's step-1 row
       const int k0 = s.kt * TK;
@@ -562,11 +588,14 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   if (p_in == t->scratch) maps.pin = t->scratch_map;
   const int ktiles = (k_hi + TK - 1) / TK;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
-  const long long units = (long long)ktiles * jtiles * (i_hi - i_lo);
+  const int chunk = chunk_planes();
+  const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
   if (grid > g.capacity) return -1;
-  const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t);
+  const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t) +
+                      sizeof(UnitRing);
+  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
   static bool attr_set[5] = {};   // per stage count: raise the dynamic smem limit once
   auto launch = [&](auto kern) {
     if (!attr_set[stages]) {
@@ -576,7 +605,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
       attr_set[stages] = true;
     }
     kern<<<(int)grid, kThreads, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
-                                           ktiles, a.omega, g, a.gosa_reset);
+                                           ktiles, chunk, a.omega, g, a.gosa_reset);
   };
   switch (stages) {
     case 2: launch(k_stencil_tma<2>); break;
@@ -602,11 +631,14 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (p_in == t->scratch) maps.pin = t->tb2_scratch;
   const int ktiles = (k_hi + TK - 1) / TK;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const long long units = (long long)ktiles * jtiles * (i_hi - i_lo);
+  const int chunk = chunk_planes();
+  const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
   if (grid > g.capacity) return -1;
-  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC) * sizeof(uint64_t);
+  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC) * sizeof(uint64_t) +
+                      sizeof(UnitRing);
+  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(k_stencil_tb2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -615,7 +647,8 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
     attr = true;
   }
   k_stencil_tb2<<<(int)grid, kThreads2, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo,
-                                                   k_hi, ktiles, a.omega, g, a.gosa_reset);
+                                                   k_hi, ktiles, chunk, a.omega, g,
+                                                   a.gosa_reset);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -52,6 +52,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// ---- device-wide dynamic work queue -----------------------------------------
+// The producer lane of each CTA claims unit ids with atomicAdd on a counter
+// (reset to 0 before the launch) and hands them to the CTA's consumer warps
+// through a small ring in shared memory (full: 1 arrive, empty: one arrive per
+// consumer warp).  A claim >= the unit count is published as kNoUnit.
+constexpr uint32_t kNoUnit = 0xffffffffu;
+constexpr int kUnitRing = 4;
+struct UnitRing {
+  uint32_t id[kUnitRing];
+  uint64_t full[kUnitRing];
+  uint64_t empty[kUnitRing];
+};
+
+__device__ __forceinline__ void unit_ring_init(UnitRing* r, int consumers);
+__device__ __forceinline__ uint32_t unit_publish(UnitRing* r, uint32_t n, unsigned int* counter,
+                                                 uint32_t units);
+__device__ __forceinline__ uint32_t unit_take(UnitRing* r, uint32_t n, int lane);
+
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
@@ -76,6 +94,33 @@ inline EncodeTiledFn encode_fn() {
       cudaGetLastError();
   }
   return fn;
+}
+
+__device__ __forceinline__ void unit_ring_init(UnitRing* r, int consumers) {
+  for (int s = 0; s < kUnitRing; ++s) {
+    mbar_init(&r->full[s], 1);
+    mbar_init(&r->empty[s], consumers);
+  }
+}
+// producer lane: claim the n-th unit of this CTA and publish it; returns the id
+__device__ __forceinline__ uint32_t unit_publish(UnitRing* r, uint32_t n, unsigned int* counter,
+                                                 uint32_t units) {
+  const int slot = n % kUnitRing;
+  if (n >= (uint32_t)kUnitRing) mbar_wait(&r->empty[slot], ((n / kUnitRing) - 1) & 1);
+  uint32_t u = atomicAdd(counter, 1u);
+  if (u >= units) u = kNoUnit;
+  r->id[slot] = u;
+  mbar_arrive(&r->full[slot]);
+  return u;
+}
+// consumer warp: the n-th unit of this CTA (all lanes), slot released by lane 0
+__device__ __forceinline__ uint32_t unit_take(UnitRing* r, uint32_t n, int lane) {
+  const int slot = n % kUnitRing;
+  mbar_wait(&r->full[slot], (n / kUnitRing) & 1);
+  const uint32_t u = *(volatile uint32_t*)&r->id[slot];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&r->empty[slot]);
+  return u;
 }
 
 // L2 promotion of a map: 0 none, 1 64B, 2 128B, 3 256B

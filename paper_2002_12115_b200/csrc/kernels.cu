@@ -121,51 +121,49 @@ __device__ __forceinline__ void nest_point(const DevFields& F, int i, int j, int
   }
 }
 
-// MAP_COLLAPSE: grid-stride over the linearised box (k fastest).
-// MAP_GANG:     block b owns outer index b of the box, threads stride the rest.
-// MAP_VECTOR:   one block strides the whole box in strips separated by barriers.
+// MAP_COLLAPSE: every warp takes whole (i, j) rows of the box (grid-stride over
+//               rows), lanes stride k -- one division per row, coalesced rows.
+// MAP_GANG:     block b owns outer index b of the box (i plane, or j row of a
+//               plane box); its warps take the rows, lanes stride k.  A row box
+//               is gang+vector over k.
+// MAP_VECTOR:   one block walks the rows in order, k strips of blockDim
+//               separated by barriers (all reads of a strip precede the next).
 template <int NEST, int MAP>
 __global__ void __launch_bounds__(kNestThreads)
 k_nest(DevFields F, Box b, LaunchArgs a, GosaSink g) {
-  const unsigned nk = (unsigned)b.nk(), nj = (unsigned)b.nj(), ni = (unsigned)b.ni();
+  const int nk = (int)b.nk(), nj = (int)b.nj(), ni = (int)b.ni();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double acc = 0.0;
   if (MAP == MAP_COLLAPSE) {
-    const unsigned long long total = (unsigned long long)ni * nj * nk;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-         t < total; t += stride) {
-      const unsigned k = (unsigned)(t % nk);
-      const unsigned long long r = t / nk;
-      const unsigned j = (unsigned)(r % nj);
-      const unsigned i = (unsigned)(r / nj);
-      nest_point<NEST>(F, b.i0 + i, b.j0 + j, b.k0 + k, a, acc);
+    const long long rows = (long long)ni * nj;
+    const long long wstride = (long long)gridDim.x * nwarps;
+    for (long long r = (long long)blockIdx.x * nwarps + warp; r < rows; r += wstride) {
+      const int i = (int)(r / nj), j = (int)(r % nj);
+      for (int k = lane; k < nk; k += 32)
+        nest_point<NEST>(F, b.i0 + i, b.j0 + j, b.k0 + k, a, acc);
     }
   } else if (MAP == MAP_GANG) {
-    // outer dimension = first non-degenerate of (i, j); a row box is gang+vector over k
     if (ni > 1) {
-      const unsigned i = blockIdx.x;
-      for (unsigned t = threadIdx.x; t < nj * nk; t += blockDim.x)
-        nest_point<NEST>(F, b.i0 + i, b.j0 + t / nk, b.k0 + t % nk, a, acc);
+      const int i = blockIdx.x;
+      for (int j = warp; j < nj; j += nwarps)
+        for (int k = lane; k < nk; k += 32)
+          nest_point<NEST>(F, b.i0 + i, b.j0 + j, b.k0 + k, a, acc);
     } else if (nj > 1) {
-      const unsigned j = blockIdx.x;
-      for (unsigned t = threadIdx.x; t < nk; t += blockDim.x)
-        nest_point<NEST>(F, b.i0, b.j0 + j, b.k0 + t, a, acc);
+      const int j = blockIdx.x;
+      for (int k = threadIdx.x; k < nk; k += blockDim.x)
+        nest_point<NEST>(F, b.i0, b.j0 + j, b.k0 + k, a, acc);
     } else {
-      const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
-      if (t < nk) nest_point<NEST>(F, b.i0, b.j0, b.k0 + t, a, acc);
+      const int k = blockIdx.x * blockDim.x + threadIdx.x;
+      if (k < nk) nest_point<NEST>(F, b.i0, b.j0, b.k0 + k, a, acc);
     }
   } else {
-    const unsigned long long total = (unsigned long long)ni * nj * nk;
-    for (unsigned long long base = 0; base < total; base += blockDim.x) {
-      const unsigned long long t = base + threadIdx.x;
-      if (t < total) {
-        const unsigned k = (unsigned)(t % nk);
-        const unsigned long long r = t / nk;
-        nest_point<NEST>(F, b.i0 + (unsigned)(r / nj), b.j0 + (unsigned)(r % nj), b.k0 + k,
-                         a, acc);
-      }
-      __syncthreads();  // strip boundary: all reads of a strip precede the next strip
-    }
+    for (int i = 0; i < ni; ++i)
+      for (int j = 0; j < nj; ++j)
+        for (int base = 0; base < nk; base += blockDim.x) {
+          const int k = base + threadIdx.x;
+          if (k < nk) nest_point<NEST>(F, b.i0 + i, b.j0 + j, b.k0 + k, a, acc);
+          __syncthreads();
+        }
   }
   if (NEST == NEST_STENCIL) gosa_commit(g, acc, gridDim.x, blockIdx.x, a.gosa_reset);
 }
@@ -409,7 +407,8 @@ int launch_nest_t(Mapping map, const DevFields& F, const Box& b, const LaunchArg
   }
   int blocks = 1;
   if (map == MAP_COLLAPSE) {
-    const long long need = (b.count() + kNestThreads - 1) / kNestThreads;
+    const long long rows = b.ni() * b.nj();
+    const long long need = (rows + kNestThreads / 32 - 1) / (kNestThreads / 32);
     blocks = (int)(need < kMaxCollapseBlocks ? need : kMaxCollapseBlocks);
   } else if (map == MAP_GANG) {
     if (b.ni() > 1) blocks = (int)b.ni();

@@ -51,6 +51,17 @@ def halo_plan(I: int, nranks: int) -> list:
     return out
 
 
+def group_nccl_id(rank: int, world: int, dist=None) -> bytes:
+    """Rank 0 creates the NCCL unique id, every rank receives it (torch.distributed)."""
+    if world <= 1:
+        return b""
+    if dist is None:
+        import torch.distributed as dist  # noqa: F811
+    obj = [N.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
 class SlabJacobi:
     """This rank's slab of a Himeno grid on one GPU; exchange over NCCL."""
 
@@ -60,14 +71,7 @@ class SlabJacobi:
         self.slab = slab_range(self.size.I, world, rank)
         sz = self.size
         self.ctx = N.Context(device, sz.I, sz.J, sz.K, slab=self.slab)
-        uid = b""
-        if world > 1:
-            if dist is None:
-                import torch.distributed as dist  # noqa: F811
-            obj = [N.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            uid = obj[0]
-        self.ctx.dd_init(world, rank, uid)
+        self.ctx.dd_init(world, rank, group_nccl_id(rank, world, dist))
         self.ctx.init_device()
 
     @property

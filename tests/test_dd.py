@@ -142,3 +142,33 @@ def test_gpu_slab_single_rank_dd(gpu):
     assert abs(s.gosa() - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
     assert np.array_equal(s.interior_p(), ref["fields"]["p"][1:sz.I - 2])
     s.close()
+
+
+def _id_main(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = dd.group_nccl_id(rank, world, dist)
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    if rank == 0:
+        q.put(ids)
+    dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_over_gloo():
+    """The NCCL id rank 0 creates (libnccl dlopen'ed by the library) reaches every rank."""
+    try:
+        N.nccl_unique_id()
+    except Exception as exc:      # no libnccl in this environment
+        pytest.skip(f"NCCL unavailable: {exc}")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + os.getpid() % 1000
+    procs = [ctx.Process(target=_id_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    ids = q.get(timeout=10)
+    assert len(ids[0]) == 128 and ids[0] == ids[1]

@@ -211,8 +211,8 @@ uint64_t hp_launch_count(hp_ctx* ctx);   /* kernels launched by this context so 
 /* Tuning sweeps: select the tuned-stencil configuration (vector width x CTAs
  * per SM, process-wide); returns the number of configurations, <0 if invalid. */
 int hp_set_stencil_config(int cfg);
-/* Two Jacobi iterations per stencil pass in the device time loop (opt-in);
- * returns the previous setting.  Default off. */
+/* Two Jacobi iterations per stencil pass in the device time loop (temporal
+ * blocking; default on); on < 0 queries; returns the previous setting. */
 int hp_set_temporal_blocking(int on);
 
 /* ---- slab decomposition over several GPUs -----------------

@@ -485,7 +485,7 @@ int stencil_grid(int cfg) {
 
 }  // namespace
 
-int g_temporal_blocking = 0;   // two-step passes (stencil_tma.cu): opt-in, see DESIGN.md §5
+int g_temporal_blocking = 1;   // two-step passes (stencil_tma.cu), DESIGN.md §5
 
 // on < 0: query only
 int set_temporal_blocking(int on) {

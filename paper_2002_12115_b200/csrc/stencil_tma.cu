@@ -46,15 +46,16 @@ constexpr uint32_t kPBytes = PW * PH * 4;                    // 5440
 constexpr uint32_t kPSlot = (kPBytes + 127) / 128 * 128;     // 5504
 constexpr uint32_t kCoefBytes = TK * TJ * 4;                 // 4096
 constexpr uint32_t kStageBytes = kPSlot + NCOEF * kCoefBytes;
-// planes per work unit (HIMENO_CHUNK overrides for sweeps)
-static int chunk_planes() {
-  static int c = 0;
-  if (!c) {
+// planes per work unit: 32 for the single-step kernel, 64 for the two-step one
+// (measured, profiles/r01_chunk_sweep.txt, r01_tb2_chunk_sweep.txt);
+// HIMENO_CHUNK overrides both for sweeps
+static int chunk_planes(int dflt) {
+  static int env = -1;
+  if (env < 0) {
     const char* e = getenv("HIMENO_CHUNK");
-    c = e ? atoi(e) : 32;
-    if (c < 1) c = 32;
+    env = e ? atoi(e) : 0;
   }
-  return c;
+  return env > 0 ? env : dflt;
 }
 
 // coefficient slots in smem order (fields a0..a3 b0..b2 c0..c2 wrk1 bnd)
@@ -254,76 +255,134 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
 
 // ================================================================ two-step kernel
 //
-// k_stencil_tb2: two Jacobi iterations per pass (temporal blocking).  Output
-// tile = TJ2 rows x 128 k; step 1 computes p1 = S(p0) on the tile extended by
-// one row / column on each side (R1 = TJ2+2 rows, 130 columns) so that step 2
-// can compute p2 = S(p1) on the tile one plane behind.  The 12 coefficient
-// arrays are read from HBM once for both iterations: 56 B per point per TWO
-// iterations (vs 2 x 56 for two single-step passes).
+// k_stencil_tb2: two Jacobi iterations per pass (temporal blocking).  A tile is
+// TJ2 output rows x TK2 = 120 output k.  Step 1 computes p1 = S(p0) on the tile
+// widened to R1 = TJ2+2 rows and QK = 128 columns (k0-4 .. k0+123: exactly 32
+// float4 quads, one per lane -- uniform SIMT, no scalar halo path); step 2
+// computes p2 = S(p1) one plane behind on the TJ2 rows, lanes 1..30 (lanes 0
+// and 31 only carry the k halo).  The 12 coefficient arrays are read from HBM
+// once for both iterations: 56 B per point per TWO iterations.
 //
-//   producer warp: p0 plane tiles (136k x (R1+2)j) into a 4-slot ring, extended
-//     coefficient tiles (136k x R1 j, 12 arrays) into a 3-slot ring.
+//   producer warp: p0 plane tiles (136k x (R1+2)j) into a 4-slot ring and the
+//     widened coefficient tiles (128k x R1 j, 12 arrays) into a 3-slot ring; work
+//     units from the device-wide queue (as k_stencil_tma).
 //   consumer warp w (0..R1-1) <-> row j0-1+w:
-//     step 1 (plane m): register queue of p0 rows, lanes = k-quads, lane 0 / 31
-//       also the extra columns k0-1 / k0+128 (scalars from the p0 ring);
-//       non-interior points copy p0 (boundaries are fixed).  p1 -> smem (2 slots).
+//     step 1 (plane m): register queue of p0 rows; non-interior points copy p0
+//       (boundaries are fixed); p1 quad -> smem (2 slots of R1 x 128).
 //     named barrier among the consumer warps (p1(m) complete)
-//     step 2 (plane m-1, warps 1..TJ2): register queue of p1 rows; coefficients
-//       of plane m-1 are still resident in the coefficient ring.
+//     step 2 (plane m-1, warps 1..TJ2): register queue of p1 rows (k+-1 by
+//       shuffles); coefficients of plane m-1 still resident in the ring.
 // Every product/sum rounds exactly like the single-step kernel: p2 is
 // bit-identical to two single steps; gosa (fp64) is that of the second step.
 constexpr int TJ2 = 6;                 // output rows per tile
-constexpr int R1 = TJ2 + 2;            // step-1 rows = consumer warps
-constexpr int kThreads2 = (R1 + 1) * 32;
-constexpr uint32_t kP0Bytes = PW * (R1 + 2) * 4;           // 5440
+constexpr int R1 = TJ2 + 2;            // step-1 rows = step-1 warps
+constexpr int TK2 = 120;               // output k per tile
+constexpr int QK = 128;                // step-1 k per tile (32 quads)
+constexpr int PW0 = QK + 8;            // p0 tile row: k0-8 .. k0+127
+constexpr int kWarps2 = R1 + TJ2 + 1;  // step-1 warps, step-2 warps, producer
+constexpr int kThreads2 = kWarps2 * 32;
+constexpr uint32_t kP0Bytes = PW0 * (R1 + 2) * 4;          // 5440
 constexpr uint32_t kP0Slot = (kP0Bytes + 127) / 128 * 128;
-constexpr uint32_t kCExtBytes = PW * R1 * 4;               // 4352 per array
-constexpr uint32_t kCSlot = NCOEF * kCExtBytes;            // 52224
-constexpr uint32_t kP1Slot = PW * R1 * 4;                  // 4352
-constexpr int SP = 4, SC = 3, SQ = 2;                      // p0 / coef / p1 ring slots
+constexpr uint32_t kCExtBytes = QK * R1 * 4;               // 4096 per array
+constexpr uint32_t kCSlot = NCOEF * kCExtBytes;            // 49152
+constexpr uint32_t kP1Slot = QK * R1 * 4;                  // 4096
+constexpr int SP = 3, SC = 4, SQ = 4;                      // p0 / coef / p1 ring slots
 constexpr uint32_t kTb2Smem = SP * kP0Slot + SC * kCSlot + SQ * kP1Slot;
 
 struct __align__(64) Tb2Maps {
-  CUtensorMap coef[NCOEF];   // box 136 x R1
-  CUtensorMap pin;           // box 136 x (R1+2)
+  CUtensorMap coef[NCOEF];   // box 128 x R1, origin (k0-4, j0-1)
+  CUtensorMap pin;           // box 136 x (R1+2), origin (k0-8, j0-2)
 };
 
-// one step of the stencil at element x of lane quads (rows: m* plane i, l* i-1, n* i+1)
-__device__ __forceinline__ float ss_point(const float* q, const Row& lm, const Row& l0,
-                                          const Row& lp, const Row& mm, const Row& m0,
-                                          const Row& mp, const Row& nm, const Row& n0,
-                                          const Row& np, int x) {
-  float s0 = fmul(q[CA0], el(n0.v, x));
-  s0 = fadd(s0, fmul(q[CA1], el(mp.v, x)));
-  s0 = fadd(s0, fmul(q[CA2], kp1(m0, x)));
-  s0 = fadd(s0, fmul(q[CB0], fadd(fsub(fsub(el(np.v, x), el(nm.v, x)), el(lp.v, x)), el(lm.v, x))));
-  s0 = fadd(s0, fmul(q[CB1], fadd(fsub(fsub(kp1(mp, x), kp1(mm, x)), km1(mp, x)), km1(mm, x))));
-  s0 = fadd(s0, fmul(q[CB2], fadd(fsub(fsub(kp1(n0, x), kp1(l0, x)), km1(n0, x)), km1(l0, x))));
-  s0 = fadd(s0, fmul(q[CC0], el(l0.v, x)));
-  s0 = fadd(s0, fmul(q[CC1], el(mm.v, x)));
-  s0 = fadd(s0, fmul(q[CC2], km1(m0, x)));
-  s0 = fadd(s0, q[CW1]);
-  return fmul(fsub(fmul(s0, q[CA3]), el(m0.v, x)), q[CBN]);
+// p0 tile row: lane quad at column 4 + 4*lane (k0-4+4*lane), edges at 3 / 132
+__device__ __forceinline__ Row load_row0(const float* ptile, int row, int lane) {
+  const float* base = ptile + row * PW0;
+  Row r;
+  r.v = *reinterpret_cast<const float4*>(base + 4 + lane * 4);
+  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1);
+  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1);
+  if (lane == 0) r.left = base[3];
+  if (lane == 31) r.right = base[4 + QK];
+  return r;
+}
+// p1 tile row (128 columns): k+-1 by shuffles only (edge lanes never output)
+__device__ __forceinline__ Row load_row1(const float* ptile, int row, int lane) {
+  Row r;
+  r.v = *reinterpret_cast<const float4*>(ptile + row * QK + lane * 4);
+  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1);
+  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1);
+  return r;
 }
 
-// the same on scalars read from shared-memory tiles: P(plane, drow, dcol)
-template <class PF>
-__device__ __forceinline__ float ss_scalar(const float* q, PF P) {
-  float s0 = fmul(q[CA0], P(1, 0, 0));
-  s0 = fadd(s0, fmul(q[CA1], P(0, 1, 0)));
-  s0 = fadd(s0, fmul(q[CA2], P(0, 0, 1)));
-  s0 = fadd(s0, fmul(q[CB0], fadd(fsub(fsub(P(1, 1, 0), P(1, -1, 0)), P(-1, 1, 0)), P(-1, -1, 0))));
-  s0 = fadd(s0, fmul(q[CB1], fadd(fsub(fsub(P(0, 1, 1), P(0, -1, 1)), P(0, 1, -1)), P(0, -1, -1))));
-  s0 = fadd(s0, fmul(q[CB2], fadd(fsub(fsub(P(1, 0, 1), P(-1, 0, 1)), P(1, 0, -1)), P(-1, 0, -1))));
-  s0 = fadd(s0, fmul(q[CC0], P(-1, 0, 0)));
-  s0 = fadd(s0, fmul(q[CC1], P(0, -1, 0)));
-  s0 = fadd(s0, fmul(q[CC2], P(0, 0, -1)));
-  s0 = fadd(s0, q[CW1]);
-  return fmul(fsub(fmul(s0, q[CA3]), P(0, 0, 0)), q[CBN]);
-}
-
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+// ss for the 4 elements of a lane quad, coefficients streamed term by term
+// from the shared-memory tile (ct = tile row base + lane quad); same order of
+// operations per element as the C program.
+__device__ __forceinline__ void ss_quad(const float* ct, const Row& lm, const Row& l0,
+                                        const Row& lp, const Row& mm, const Row& m0,
+                                        const Row& mp, const Row& nm, const Row& n0,
+                                        const Row& np, float (&ss)[4]) {
+  constexpr int CS = QK * R1;   // stride between coefficient arrays in the tile
+  auto Q = [&](int c) { return *reinterpret_cast<const float4*>(ct + c * CS); };
+  float s0[4];
+  {
+    const float4 q = Q(CA0);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fmul(el(q, x), el(n0.v, x));
+  }
+  {
+    const float4 q = Q(CA1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), el(mp.v, x)));
+  }
+  {
+    const float4 q = Q(CA2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), kp1(m0, x)));
+  }
+  {
+    const float4 q = Q(CB0);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      s0[x] = fadd(s0[x], fmul(el(q, x), fadd(fsub(fsub(el(np.v, x), el(nm.v, x)), el(lp.v, x)),
+                                              el(lm.v, x))));
+  }
+  {
+    const float4 q = Q(CB1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      s0[x] = fadd(s0[x], fmul(el(q, x), fadd(fsub(fsub(kp1(mp, x), kp1(mm, x)), km1(mp, x)),
+                                              km1(mm, x))));
+  }
+  {
+    const float4 q = Q(CB2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      s0[x] = fadd(s0[x], fmul(el(q, x), fadd(fsub(fsub(kp1(n0, x), kp1(l0, x)), km1(n0, x)),
+                                              km1(l0, x))));
+  }
+  {
+    const float4 q = Q(CC0);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), el(l0.v, x)));
+  }
+  {
+    const float4 q = Q(CC1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), el(mm.v, x)));
+  }
+  {
+    const float4 q = Q(CC2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), km1(m0, x)));
+  }
+  {
+    const float4 q = Q(CW1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], el(q, x));
+  }
+  const float4 a3 = Q(CA3), bn = Q(CBN);
+#pragma unroll
+  for (int x = 0; x < 4; ++x) ss[x] = fmul(fsub(fmul(s0[x], el(a3, x)), el(m0.v, x)), el(bn, x));
 }
 
 __global__ void __launch_bounds__(kThreads2, 1)
@@ -340,7 +399,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   uint64_t* pempty = pfull + SP;
   uint64_t* cfull = pempty + SP;
   uint64_t* cempty = cfull + SC;
-  UnitRing* ring = reinterpret_cast<UnitRing*>(cempty + SC);
+  uint64_t* qfull = cempty + SC;
+  uint64_t* qempty = qfull + SQ;
+  UnitRing* ring = reinterpret_cast<UnitRing*>(qempty + SQ);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
@@ -348,174 +409,176 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
               (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], R1); }
-    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1); }
-    unit_ring_init(ring, R1);
+    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1 + TJ2); }
+    for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], R1); mbar_init(&qempty[s], TJ2); }
+    unit_ring_init(ring, R1 + TJ2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   double acc = 0.0;
-  if (warp == R1) {
+  if (warp == R1 + TJ2) {
     // ------------------------------------------------------------- producer
     if (lane == 0) {
       uint32_t sp = 0, sc = 0;
       Unit s{0, 0, 0, 0};
-      auto load_p0 = [&](const Unit& u, int plane) {
-        const int slot = sp % SP;
-        if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
-        mbar_expect_tx(&pfull[slot], kP0Bytes);
-        tma_load_3d(p0ring + slot * kP0Slot, &maps.pin, &pfull[slot], u.kt * TK - 4,
-                    j_lo + u.jt * TJ2 - 2, plane);
-        ++sp;
-      };
-      auto load_c = [&](const Unit& u, int plane) {
-        const int slot = sc % SC;
-        if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
-        mbar_expect_tx(&cfull[slot], NCOEF * kCExtBytes);
-        for (int m = 0; m < NCOEF; ++m)
-          tma_load_3d(cring + slot * kCSlot + m * kCExtBytes, &maps.coef[m], &cfull[slot],
-                      u.kt * TK - 4, j_lo + u.jt * TJ2 - 1, plane);
-        ++sc;
-      };
       for (uint32_t n = 0;; ++n) {
         const uint32_t u = unit_publish(ring, n, g.work, units.count);
         if (u == kNoUnit) break;
         units.decode(u, s);
         const int ia = i_lo + s.ia, ib = i_lo + s.ib;
-        load_p0(s, ia - 2);
-        load_p0(s, ia - 1);
+        const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+        auto load_p0 = [&](int plane) {
+          const int slot = sp % SP;
+          if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
+          mbar_expect_tx(&pfull[slot], kP0Bytes);
+          tma_load_3d(p0ring + slot * kP0Slot, &maps.pin, &pfull[slot], k0 - 8, j0 - 2, plane);
+          ++sp;
+        };
+        load_p0(ia - 2);
+        load_p0(ia - 1);
         for (int m = ia - 1; m <= ib; ++m) {
-          load_p0(s, m + 1);
-          load_c(s, m);
+          load_p0(m + 1);
+          const int slot = sc % SC;
+          if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
+          mbar_expect_tx(&cfull[slot], NCOEF * kCExtBytes);
+          for (int c = 0; c < NCOEF; ++c)
+            tma_load_3d(cring + slot * kCSlot + c * kCExtBytes, &maps.coef[c], &cfull[slot],
+                        k0 - 4, j0 - 1, m);
+          ++sc;
         }
       }
     }
-  } else {
-    // ------------------------------------------------------------ consumers
-    uint32_t sp = 0, sc = 0;   // consumed counts of the two rings
-    uint32_t it = 0;           // p1 slot counter
+  } else if (warp < R1) {
+    // ------------------------------------------------ step-1 warps (row j0-1+w)
+    uint32_t sp = 0, sc = 0, sq = 0;
     Unit s;
-    const int imax1 = i_hi;    // planes [i_lo, i_hi) are the global interior
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
       if (u == kNoUnit) break;
       units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
-      const int j1 = j_lo + s.jt * TJ2 - 1 + warp;      // this warp's step-1 row
-      const int k0 = s.kt * TK;
-      const int kb = k0 + lane * 4;
+      const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+      const int j1 = j0 - 1 + warp;
+      const int kq = k0 - 4 + lane * 4;
       const bool row_in = j1 >= j_lo && j1 < j_hi;
       bool in1[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) in1[x] = row_in && kb + x >= k_lo && kb + x < k_hi;
-      const bool out_row = warp >= 1 && warp <= TJ2 && row_in;   // step-2 output row
-      // p0 queue: planes m-1 (a*), m (b*); p0 slot of plane q = sequence sp0 + (q - (ia-2))
-      const uint32_t sp0 = sp;
+      for (int x = 0; x < 4; ++x) in1[x] = row_in && kq + x >= k_lo && kq + x < k_hi;
       Row am, a0, ap, bm, b0, bp;
       for (int w = 0; w < 2; ++w) {
         const int slot = sp % SP;
         mbar_wait(&pfull[slot], (sp / SP) & 1);
         const float* pt = reinterpret_cast<const float*>(p0ring + slot * kP0Slot);
-        const Row x0 = load_row(pt, warp, lane), x1 = load_row(pt, warp + 1, lane),
-                  x2 = load_row(pt, warp + 2, lane);
+        const Row x0 = load_row0(pt, warp, lane), x1 = load_row0(pt, warp + 1, lane),
+                  x2 = load_row0(pt, warp + 2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[slot]);
         if (w == 0) { am = x0; a0 = x1; ap = x2; } else { bm = x0; b0 = x1; bp = x2; }
         ++sp;
       }
-      // first p0 plane (ia-2) is only needed by step1(ia-1)'s scalars: released in-loop
-      Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
+#pragma unroll 1
       for (int m = ia - 1; m <= ib; ++m) {
         const int pslot = sp % SP;
         mbar_wait(&pfull[pslot], (sp / SP) & 1);
         const float* pt = reinterpret_cast<const float*>(p0ring + pslot * kP0Slot);
-        const Row cm = load_row(pt, warp, lane), c0 = load_row(pt, warp + 1, lane),
-                  cp = load_row(pt, warp + 2, lane);
+        const Row cm = load_row0(pt, warp, lane), c0 = load_row0(pt, warp + 1, lane),
+                  cp = load_row0(pt, warp + 2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[pslot]);
         ++sp;
         const int cslot = sc % SC;
         mbar_wait(&cfull[cslot], (sc / SC) & 1);
-        ++sc;
-        const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot);
-        // ---- step 1 at plane m, row j1 -> p1 slot
-        float* q1 = p1ring + (it % SQ) * (PW * R1);
-        const bool plane_in = m >= i_lo && m < imax1;
+        const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot) + warp * QK + lane * 4;
+        const bool plane_in = m >= i_lo && m < i_hi;
         float r[4];
-        float qv[4][NCOEF];
+        if (plane_in && row_in) {
+          float ss[4];
+          ss_quad(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
 #pragma unroll
-        for (int c = 0; c < NCOEF; ++c) {
-          const float4 t = *reinterpret_cast<const float4*>(ct + c * (PW * R1) + warp * PW + 4 + lane * 4);
-          qv[0][c] = t.x; qv[1][c] = t.y; qv[2][c] = t.z; qv[3][c] = t.w;
-        }
+          for (int x = 0; x < 4; ++x) r[x] = in1[x] ? fadd(el(b0.v, x), fmul(omega, ss[x])) : el(b0.v, x);
+        } else {
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-          r[x] = (plane_in && in1[x]) ? fadd(el(b0.v, x), fmul(omega, ss_point(qv[x], am, a0, ap,
-                                                                                  bm, b0, bp, cm,
-                                                                                  c0, cp, x)))
-                                      : el(b0.v, x);
-        *reinterpret_cast<float4*>(q1 + warp * PW + 4 + lane * 4) = make_float4(r[0], r[1], r[2], r[3]);
-        if (lane == 0 || lane == 31) {
-          // extra column k0-1 (lane 0) / k0+128 (lane 31), scalars from the p0 ring
-          const int col = lane == 0 ? 3 : 4 + TK;
-          const int k = k0 - 4 + col;
-          const float* pl[3];
-          for (int d = 0; d < 3; ++d)
-            pl[d] = reinterpret_cast<const float*>(p0ring + ((sp0 + (m - (ia - 2)) - 1 + d) % SP) * kP0Slot);
-          auto P = [&](int di, int dj, int dk) { return pl[di + 1][(warp + 1 + dj) * PW + col + dk]; };
-          float v = P(0, 0, 0);
-          if (plane_in && row_in && k >= k_lo && k < k_hi) {
-            float qs[NCOEF];
-            for (int c = 0; c < NCOEF; ++c) qs[c] = ct[c * (PW * R1) + warp * PW + col];
-            v = fadd(v, fmul(omega, ss_scalar(qs, P)));
-          }
-          q1[warp * PW + col] = v;
+          for (int x = 0; x < 4; ++x) r[x] = el(b0.v, x);
         }
-        // p0 plane m-1 is no longer needed (scalars of step1(m) were its last use)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[(sp0 + (m - (ia - 2)) - 1) % SP]);
-        named_bar(1, R1 * 32);
-        // ---- p1(m) rows into the queue; step 2 at plane m-1
-        const Row nm = load_row(q1, warp > 0 ? warp - 1 : 0, lane),
-                  n0 = load_row(q1, warp, lane),
-                  np = load_row(q1, warp < R1 - 1 ? warp + 1 : R1 - 1, lane);
-        if (m >= ia + 1 && out_row) {
-          const int pc = (sc - 2) % SC;   // coefficient slot of plane m-1
-          const float* cq = reinterpret_cast<const float*>(cring + pc * kCSlot);
-          float q2[4][NCOEF];
-#pragma unroll
-          for (int c = 0; c < NCOEF; ++c) {
-            const float4 t = *reinterpret_cast<const float4*>(cq + c * (PW * R1) + warp * PW + 4 + lane * 4);
-            q2[0][c] = t.x; q2[1][c] = t.y; q2[2][c] = t.z; q2[3][c] = t.w;
-          }
-          float w2[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const float ss = ss_point(q2[x], ym, y0, yp, zm, z0, zp, nm, n0, np, x);
-            w2[x] = fadd(el(z0.v, x), fmul(omega, ss));
-            if (in1[x]) acc += (double)fmul(ss, ss);
-          }
-          float* o = out + F.at(m - 1, j1, kb);
-          if (in1[0] && in1[1] && in1[2] && in1[3]) {
-            *reinterpret_cast<float4*>(o) = make_float4(w2[0], w2[1], w2[2], w2[3]);
-          } else {
-            for (int x = 0; x < 4; ++x)
-              if (in1[x]) o[x] = w2[x];
-          }
-        }
-        // release coefficient stages: plane m-1 after its step 2, plane ia-1 / ib after step 1
+        if (lane == 0) mbar_arrive(&cempty[cslot]);
+        ++sc;
+        // p1(m) -> ring slot (wait until the step-2 warps released its last use)
+        const int qslot = sq % SQ;
+        if (sq >= (uint32_t)SQ) mbar_wait(&qempty[qslot], ((sq / SQ) - 1) & 1);
+        float* q1 = p1ring + qslot * (QK * R1);
+        *reinterpret_cast<float4*>(q1 + warp * QK + lane * 4) = make_float4(r[0], r[1], r[2], r[3]);
         __syncwarp();
-        if (lane == 0) {
-          if (m >= ia + 1) mbar_arrive(&cempty[(sc - 2) % SC]);
-          if (m == ia - 1 || m == ib) mbar_arrive(&cempty[(sc - 1) % SC]);
-        }
-        ym = zm; y0 = z0; yp = zp;
-        zm = nm; z0 = n0; zp = np;
+        if (lane == 0) mbar_arrive(&qfull[qslot]);   // release semantics publish the row
+        ++sq;
         am = bm; a0 = b0; ap = bp;
         bm = cm; b0 = c0; bp = cp;
-        ++it;
       }
-      // release the p0 planes ib and ib+1 (and nothing else remains)
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&pempty[(sp - 2) % SP]);
-        mbar_arrive(&pempty[(sp - 1) % SP]);
+    }
+  } else {
+    // ------------------------------------------ step-2 warps (output row j0+w2)
+    const int w2 = warp - R1;
+    uint32_t sc = 0, sq = 0;
+    Unit s;
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t u = unit_take(ring, n, lane);
+      if (u == kNoUnit) break;
+      units.decode(u, s);
+      const int ia = i_lo + s.ia, ib = i_lo + s.ib;
+      const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+      const int j = j0 + w2;
+      const int kq = k0 - 4 + lane * 4;
+      const bool row_in = j < j_hi;
+      bool in2[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) in2[x] = row_in && kq + x >= k_lo && kq + x < k_hi;
+      const bool writer = row_in && lane >= 1 && lane <= 30;
+      Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
+#pragma unroll 1
+      for (int m = ia - 1; m <= ib; ++m) {
+        const int qslot = sq % SQ;
+        mbar_wait(&qfull[qslot], (sq / SQ) & 1);
+        const float* q1 = p1ring + qslot * (QK * R1);
+        const Row nm = load_row1(q1, w2, lane), n0 = load_row1(q1, w2 + 1, lane),
+                  np = load_row1(q1, w2 + 2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[qslot]);
+        ++sq;
+        // coefficient stage of plane m (sequence sc): used at iteration m+1 for
+        // output plane m; stages of planes ia-1 and ib are only released
+        if (m >= ia + 1) {
+          const int cslot = (sc - 1) % SC;          // stage of plane m-1
+          mbar_wait(&cfull[cslot], ((sc - 1) / SC) & 1);
+          const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot) + (w2 + 1) * QK + lane * 4;
+          float ss[4];
+          ss_quad(ct, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
+          float w[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            w[x] = fadd(el(z0.v, x), fmul(omega, ss[x]));
+            if (writer && in2[x]) acc += (double)fmul(ss[x], ss[x]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&cempty[cslot]);
+          if (writer) {
+            float* o = out + F.at(m - 1, j, kq);
+            if (in2[0] && in2[1] && in2[2] && in2[3]) {
+              *reinterpret_cast<float4*>(o) = make_float4(w[0], w[1], w[2], w[3]);
+            } else {
+              for (int x = 0; x < 4; ++x)
+                if (in2[x]) o[x] = w[x];
+            }
+          }
+        } else if (m == ia) {
+          // stage of plane ia-1 carries no output plane: release it unused
+          if (lane == 0) mbar_arrive(&cempty[(sc - 1) % SC]);
+        }
+        ++sc;   // stage of plane m
+        ym = zm; y0 = z0; yp = zp;
+        zm = nm; z0 = n0; zp = np;
       }
+      // stage of plane ib carries no output plane either
+      if (lane == 0) mbar_arrive(&cempty[(sc - 1) % SC]);
     }
   }
   gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
@@ -539,7 +602,7 @@ struct TmaState {
 // HIMENO_TMA_PROMO="a,b,c,d": L2 promotion codes (0 none, 1 64B, 2 128B, 3 256B)
 // of the single-step coefficient / p maps and the two-step coefficient / p maps.
 static void promo_codes(int* c) {
-  c[0] = 2; c[1] = 2; c[2] = 0; c[3] = 0;
+  c[0] = 2; c[1] = 2; c[2] = 2; c[3] = 2;
   if (const char* e = getenv("HIMENO_TMA_PROMO"))
     sscanf(e, "%d,%d,%d,%d", &c[0], &c[1], &c[2], &c[3]);
 }
@@ -559,10 +622,10 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   for (int m = 0; m < NCOEF; ++m) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    ok = ok && encode(&t->tb2.coef[m], F, F.f[fields[m]], PW, R1, pc[2]);
+    ok = ok && encode(&t->tb2.coef[m], F, F.f[fields[m]], QK, R1, pc[2]);
   }
-  ok = ok && encode(&t->tb2.pin, F, F.f[HP_F_P], PW, R1 + 2, pc[3]);
-  ok = ok && encode(&t->tb2_scratch, F, scratch, PW, R1 + 2, pc[3]);
+  ok = ok && encode(&t->tb2.pin, F, F.f[HP_F_P], PW0, R1 + 2, pc[3]);
+  ok = ok && encode(&t->tb2_scratch, F, scratch, PW0, R1 + 2, pc[3]);
   t->p = F.f[HP_F_P];
   t->scratch = scratch;
   if (!ok) {
@@ -588,7 +651,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   if (p_in == t->scratch) maps.pin = t->scratch_map;
   const int ktiles = (k_hi + TK - 1) / TK;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
-  const int chunk = chunk_planes();
+  const int chunk = chunk_planes(32);
   const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
@@ -629,14 +692,14 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   Tb2Maps maps = t->tb2;
   if (p_in == t->scratch) maps.pin = t->tb2_scratch;
-  const int ktiles = (k_hi + TK - 1) / TK;
+  const int ktiles = (k_hi + TK2 - 1) / TK2;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const int chunk = chunk_planes();
+  const int chunk = chunk_planes(64);
   const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
   if (grid > g.capacity) return -1;
-  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC) * sizeof(uint64_t) +
+  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC + SQ) * sizeof(uint64_t) +
                       sizeof(UnitRing);
   if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
   static bool attr = false;

@@ -261,17 +261,24 @@ def run_ours(args, world, rank, local):
     peak, peak_src = peaks()
     points = slab.interior_points if slab is not None else size.interior_points
     achieved = BYTES_STENCIL * points / (kt.stencil_ms / 1e3) / 1e9
-    traffic = None
+    # DRAM bytes per launch from the committed ncu capture of the same kernel (L grid)
+    ncu_kernels = {}
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("stencil_dram_bytes_per_launch")
+            ncu_kernels = json.loads(prof.read_text()).get("kernels", {})
         except ValueError:
-            traffic = None
+            ncu_kernels = {}
+    key_tb, key_1 = "k_stencil_tb2", "k_stencil_tma<3>"
+    on_l = size.name == "L" and slab is None
+    traffic = (ncu_kernels.get(key_tb if kt.stencil_iters > 1.5 else key_1, {})
+               .get("dram_bytes_per_launch") if on_l else None)
+    traffic1 = ncu_kernels.get(key_1, {}).get("dram_bytes_per_launch") if on_l else None
     achieved1 = BYTES_STENCIL * points / (kt1.stencil_ms / 1e3) / 1e9
     roofline_single = {"bound": "hbm", "achieved": achieved1, "peak": peak, "unit": "GB/s",
                        "frac": achieved1 / peak, "kernel": "k_stencil_tma<3> (one iteration per pass)",
                        "launch_ms": kt1.stencil_ms, "iterations_per_launch": kt1.stencil_iters,
+                       "traffic": traffic1,
                        "gflops": FLOP_PER_POINT * points * kt1.stencil_iters / kt1.stencil_ms / 1e6}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,

@@ -176,9 +176,10 @@ int hp_read_gosa(hp_ctx* ctx, int side, double* out);
 
 /* ---- device-resident Jacobi (bench value / e2e) ----------------------------
  * hp_jacobi_device: nn iterations of jacobi's loop body on the device mirrors,
- * enqueued on hp_stream(ctx) without host synchronisation.  variant: 0 = the
- * kernels selected for pattern 0000001000000 (stencil_3d + copy_3d),
- * 1 = fused time loop (p/wrk2 rotation, copy nest elided, 56 B/pt).
+ * enqueued on hp_stream(ctx) without host synchronisation.  variant: 0 = one
+ * stencil + one copy launch per iteration (the unfused loop body), 1 = fused
+ * time loop (p/wrk2 rotation, copy nest elided; two iterations per stencil
+ * pass while temporal blocking is on).
  * hp_jacobi_host: end-to-end offload of jacobi(nn) from host buffers: H2D of
  * the 13 input fields (fields[HP_F_*], wrk2 ignored), the device loop, D2H of
  * p into p_out and gosa into *gosa_out; synchronous.  Host buffers may be
@@ -188,10 +189,6 @@ int hp_jacobi_host(hp_ctx* ctx, const float* const* fields, int nn, int variant,
                    float* p_out, double* gosa_out);
 /* Initialise the device mirrors to the program's post-initmt state on device. */
 int hp_init_device(hp_ctx* ctx);
-/* Launch-level timing of the last hp_jacobi_device call region: the caller
- * records its own events on hp_stream(); this helper reports the stream id's
- * kernel count per iteration for the given variant. */
-int hp_launches_per_iteration(int variant);
 
 /* ---- device timing (bench.py) ----------------------------------------------
  * hp_time_steps: CUDA events on hp_stream(ctx) around `steps` back-to-back

@@ -1026,7 +1026,6 @@ extern "C" int hp_read_gosa(hp_ctx* c, int side, double* out) {
 
 static LaunchArgs default_args(const hp_ctx* c, int reset) { return ctx_args(c, reset); }
 
-extern "C" int hp_launches_per_iteration(int variant) { return variant == 1 ? 1 : 2; }
 
 extern "C" int hp_init_device(hp_ctx* c) {
   if (!c) return HP_ERR_ARG;

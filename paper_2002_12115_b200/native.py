@@ -98,7 +98,6 @@ SIGNATURES = {
     "hp_jacobi_host": (C.c_int, [_CtxP, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                  C.c_void_p, C.POINTER(C.c_double)]),
     "hp_init_device": (C.c_int, [_CtxP]),
-    "hp_launches_per_iteration": (C.c_int, [C.c_int]),
     "hp_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "hp_time_jacobi": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(KernelTimes)]),
     "hp_launch_count": (C.c_uint64, [_CtxP]),

@@ -218,3 +218,24 @@ def test_concurrent_workers_share_a_device(gpu):
             assert abs(st["gosa"] - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], g
             assert st["n_stale_reads"] == 0
         assert len(ev._contexts) == 3
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+def test_headline_L_grid_bit_exact(gpu, tb):
+    """The bench workload's grid (L), both time-loop kernels, against the oracle."""
+    sz = himeno.size("L")
+    nn = 3
+    f = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(f)
+    g64, _ = oracle.jacobi(f, nn, threads=oracle.max_threads())
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    assert np.array_equal(p, f["p"])
+    assert abs(g - g64) <= 1e-11 * g64     # threaded oracle sums planes in another order

@@ -410,7 +410,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], R1); }
     for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1 + TJ2); }
-    for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], R1); mbar_init(&qempty[s], TJ2); }
+    // p1 ring: every thread arrives (no reliance on __syncwarp ordering for the
+    // shared-memory rows written / read by other warps)
+    for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], R1 * 32); mbar_init(&qempty[s], TJ2 * 32); }
     unit_ring_init(ring, R1 + TJ2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -508,8 +510,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         if (sq >= (uint32_t)SQ) mbar_wait(&qempty[qslot], ((sq / SQ) - 1) & 1);
         float* q1 = p1ring + qslot * (QK * R1);
         *reinterpret_cast<float4*>(q1 + warp * QK + lane * 4) = make_float4(r[0], r[1], r[2], r[3]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&qfull[qslot]);   // release semantics publish the row
+        mbar_arrive(&qfull[qslot]);   // release: publishes this thread's quad
         ++sq;
         am = bm; a0 = b0; ap = bp;
         bm = cm; b0 = c0; bp = cp;
@@ -541,8 +542,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         const float* q1 = p1ring + qslot * (QK * R1);
         const Row nm = load_row1(q1, w2, lane), n0 = load_row1(q1, w2 + 1, lane),
                   np = load_row1(q1, w2 + 2, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&qempty[qslot]);
+        mbar_arrive(&qempty[qslot]);  // this thread's reads of the slot are done
         ++sq;
         // coefficient stage of plane m (sequence sc): used at iteration m+1 for
         // output plane m; stages of planes ia-1 and ib are only released

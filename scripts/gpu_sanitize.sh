@@ -1,0 +1,9 @@
+#!/bin/bash
+TAG=${1:-sanitize}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_run.py > $OUT/$tool.log 2>&1
+  echo "$tool rc=$?" >> $OUT/$tool.log
+  echo "== $tool"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|rc=|Error" $OUT/$tool.log | head -5
+done

@@ -1,0 +1,30 @@
+"""Small workload exercising every kernel family, for compute-sanitizer runs."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2002_12115_b200 import native as N  # noqa: E402
+from paper_2002_12115_b200.apps import himeno  # noqa: E402
+from paper_2002_12115_b200.evaluator import B200Evaluator  # noqa: E402
+from paper_2002_12115_b200.kinds import DirectiveKind  # noqa: E402
+
+lib = N.load()
+sz = himeno.custom_size(20, 29, 300)
+for tb in (0, 1):
+    lib.hp_set_temporal_blocking(tb)
+    with N.Context(0, sz.I, sz.J, sz.K) as c:
+        c.init_device()
+        c.jacobi_device(3, 1)
+        c.jacobi_device(2, 0)
+        print("device jacobi tb", tb, c.read_gosa(1))
+lib.hp_set_temporal_blocking(1)
+with B200Evaluator("XXS", nn=2) as ev:
+    for g in ("0000000100100", "0010010010010", "0100100100100", "1001001000000",
+              "0000001000000", "0000000000001"):
+        print(g, ev.measure(tuple(int(x) for x in g)))
+prog = himeno.program()
+with B200Evaluator("XXS", nn=2, kinds={l: DirectiveKind.PARALLEL_LOOP_VECTOR for l in prog.kinds}) as ev:
+    print("plv", ev.measure((0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0)))
+from paper_2002_12115_b200 import dd  # noqa: E402
+with dd.GroupJacobi("XS", [0, 0, 0]) as g:
+    print("group", g.jacobi(2))

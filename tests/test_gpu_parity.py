@@ -239,3 +239,33 @@ def test_headline_L_grid_bit_exact(gpu, tb):
         lib.hp_set_temporal_blocking(old)
     assert np.array_equal(p, f["p"])
     assert abs(g - g64) <= 1e-11 * g64     # threaded oracle sums planes in another order
+
+
+@pytest.mark.parametrize("dims", [(4, 4, 4), (5, 4, 9), (4, 7, 5), (6, 6, 6), (9, 5, 133)])
+def test_tiny_and_ragged_grids_all_genomes(gpu, dims):
+    """Minimal / ragged grids (one interior point, partial tiles) for every runnable genome."""
+    sz = himeno.custom_size(*dims)
+    for nn in (1, 2, 3):
+        ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+        with B200Evaluator(sz, nn=nn, poison_device=True) as ev:
+            for g in valid_genomes(ev.loops, ev.eligible_ids)[::7]:
+                res = ev.run(g)
+                p = ev.read_field("p", side=0)
+                assert np.array_equal(p, ref["fields"]["p"]), (dims, nn, g)
+                assert abs(res.gosa - ref["gosa64"]) <= GOSA_RTOL * max(ref["gosa64"], 1e-300), \
+                    (dims, nn, g, res.gosa, ref["gosa64"])
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+def test_device_jacobi_zero_iterations(gpu, tb):
+    sz = himeno.size("XS")
+    ref = oracle.run_program(sz.I, sz.J, sz.K, 0)
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(0, 1)
+            assert np.array_equal(ctx.read_field("p", 1), ref["fields"]["p"])
+    finally:
+        lib.hp_set_temporal_blocking(old)

@@ -1,0 +1,172 @@
+"""The tuning pipeline on the B200 evaluator: baseline -> GA -> best plan -> verification -> report.
+
+Mirrors the reference's ``run_pipeline`` (acctuner/cli.py:211-284) for the hot path:
+``measure_baseline`` (cli.py:200-208), ``run_ga`` (ga.py:183-211), the numeric output
+diff ``verify_results`` (cli.py:155-186; defaults atol 1e-6, rtol 1e-4, cli.py:34-35)
+between the all-CPU program's stdout and the best pattern's, and the report files
+(``report.json`` with the reference's keys, ``generations.jsonl``, ``meta.json``;
+cli.py:287-317).  Front-end stages (parse/classify) are replaced by the committed
+program model (apps/model/himeno.json).
+
+    python -m paper_2002_12115_b200.tune --size M --nn 3 --population 20 \\
+        --generations 20 --devices all --out tune-out
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import platform
+import sys
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional
+
+from . import ga
+from .errors import UnparsableOutput
+from .evaluator import B200Evaluator, measure_baseline
+
+DEFAULT_ATOL = 1e-6
+DEFAULT_RTOL = 1e-4
+
+
+@dataclass
+class DiffReport:
+    passed: bool
+    values_compared: int
+    max_abs_err: float
+    max_rel_err: float
+    mismatches: int
+    atol: float
+    rtol: float
+    length_mismatch: bool = False
+    detail: list = field(default_factory=list)
+
+    def to_json(self) -> dict:
+        return {"passed": self.passed, "values_compared": self.values_compared,
+                "max_abs_err": self.max_abs_err, "max_rel_err": self.max_rel_err,
+                "mismatches": self.mismatches, "atol": self.atol, "rtol": self.rtol,
+                "length_mismatch": self.length_mismatch, "detail": self.detail[:10]}
+
+
+def _number(token: str) -> Optional[float]:
+    try:
+        return float(token)
+    except ValueError:
+        return None
+
+
+def verify_results(baseline_output: str, tuned_output: str, atol: float = DEFAULT_ATOL,
+                   rtol: float = DEFAULT_RTOL) -> DiffReport:
+    """Whitespace-token numeric diff: pass iff |t - b| <= atol + rtol*|b| for every value;
+    non-numeric tokens must match exactly; different token counts fail."""
+    if not isinstance(baseline_output, str) or not isinstance(tuned_output, str):
+        raise UnparsableOutput("output streams must be text")
+    base, tuned = baseline_output.split(), tuned_output.split()
+    rep = DiffReport(True, 0, 0.0, 0.0, 0, atol, rtol)
+    if len(base) != len(tuned):
+        rep.passed = False
+        rep.length_mismatch = True
+        rep.detail.append(f"value counts differ: {len(base)} vs {len(tuned)}")
+    for idx, (b, t) in enumerate(zip(base, tuned)):
+        rep.values_compared += 1
+        fb, ft = _number(b), _number(t)
+        if fb is None or ft is None:
+            if b != t:
+                rep.mismatches += 1
+                rep.passed = False
+                rep.detail.append(f"token {idx}: {t!r} != {b!r}")
+            continue
+        abs_err = abs(ft - fb)
+        rel_err = abs_err / abs(fb) if fb != 0 else (0.0 if abs_err == 0 else float("inf"))
+        rep.max_abs_err = max(rep.max_abs_err, abs_err)
+        rep.max_rel_err = max(rep.max_rel_err, rel_err)
+        if abs_err > atol + rtol * abs(fb):
+            rep.mismatches += 1
+            rep.passed = False
+            if len(rep.detail) < 10:
+                rep.detail.append(f"value {idx}: {ft!r} vs {fb!r} (abs {abs_err:.3e})")
+    return rep
+
+
+def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
+               atol: float = DEFAULT_ATOL, rtol: float = DEFAULT_RTOL, echo=print) -> tuple:
+    """Baseline, GA, verification and reports; returns (report document, verification ok)."""
+    gene_len = evaluator.gene_length
+    echo(f"gene length {gene_len}; evaluator: B200 x {evaluator.max_concurrency} worker slot(s), "
+         f"Himeno {evaluator.size.name} {evaluator.size.I}x{evaluator.size.J}x{evaluator.size.K}, "
+         f"nn={evaluator.nn}")
+    t0 = time.perf_counter()
+    baseline_s = measure_baseline(evaluator, gene_len)
+    echo(f"baseline (all-CPU) time: {baseline_s:.6g} s")
+
+    def on_generation(rec):
+        echo(f"generation {rec.generation}: best so far {rec.best_time_s:.6g} s")
+
+    result = ga.run_ga(config, gene_len, evaluator, on_generation)
+    best = result.best
+    ratio = baseline_s / best.time_s
+    echo(f"best genome {ga.genome_str(best.genome)} time {best.time_s:.6g} s "
+         f"ratio {ratio:.3f}x ({result.evaluations} evaluations)")
+    base_out = evaluator.run_for_output((0,) * gene_len)
+    tuned_out = evaluator.run_for_output(best.genome)
+    diff = verify_results(base_out, tuned_out, atol, rtol)
+    echo(f"verification: {'pass' if diff.passed else 'FAIL'} (max abs err {diff.max_abs_err:.3e})")
+    plan = evaluator.plan(best.genome)
+    report = {
+        "baseline_time_s": baseline_s,
+        "best_time_s": best.time_s,
+        "improvement_ratio": ratio,
+        "best_genome": ga.genome_str(best.genome),
+        "gene_length": gene_len,
+        "kinds": {str(l): evaluator.kinds[l].value for l in evaluator.eligible_ids},
+        "plan": plan.to_json(evaluator.refs),
+        "verification": diff.to_json() | {"status": "ran"},
+        "evaluations": result.evaluations,
+        "ga": {"population": config.population, "generations": config.generations,
+               "crossover_rate": config.crossover_rate, "mutation_rate": config.mutation_rate,
+               "rng_seed": config.rng_seed},
+        "note": "",
+        "b200": {"best_run": evaluator.stats.get(best.genome, {}),
+                 "worker_slots": evaluator.max_concurrency,
+                 "transfer_mode": evaluator.transfer_mode,
+                 "wall_s": time.perf_counter() - t0},
+    }
+    if out_dir is not None:
+        out = Path(out_dir)
+        out.mkdir(parents=True, exist_ok=True)
+        (out / "report.json").write_text(json.dumps(report, indent=2, sort_keys=True) + "\n")
+        with (out / "generations.jsonl").open("w") as fh:
+            for rec in result.records:
+                fh.write(json.dumps(rec.to_json(), sort_keys=True) + "\n")
+        meta = {"written_at": time.strftime("%Y-%m-%dT%H:%M:%S%z"), "host": platform.node(),
+                "python": platform.python_version()}
+        (out / "meta.json").write_text(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+    return report, diff.passed
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description="GA offload search on B200s (Himeno)")
+    ap.add_argument("--size", default="M")
+    ap.add_argument("--nn", type=int, default=3)
+    ap.add_argument("--population", type=int, default=10)
+    ap.add_argument("--generations", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--devices", default="0", help="comma list of GPU ids, or 'all'")
+    ap.add_argument("--workers-per-device", type=int, default=1)
+    ap.add_argument("--transfer-mode", default="batched", choices=["batched", "per-loop"])
+    ap.add_argument("--out")
+    args = ap.parse_args(argv)
+    devices = "all" if args.devices == "all" else [int(d) for d in args.devices.split(",")]
+    cfg = ga.GAConfig(population=args.population, generations=args.generations,
+                      rng_seed=args.seed)
+    with B200Evaluator(args.size, nn=args.nn, devices=devices,
+                       workers_per_device=args.workers_per_device,
+                       transfer_mode=args.transfer_mode) as ev:
+        _report, ok = run_tuning(ev, cfg, args.out)
+    return 0 if ok else 3
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,42 @@
+"""Pipeline pieces: verify_results parity with the reference; a GPU tuning run."""
+import json
+
+import pytest
+
+from paper_2002_12115_b200 import ga
+from paper_2002_12115_b200.tune import verify_results
+
+CASES = [("1.0 2.0 3.0", "1.0 2.0 3.0"), ("1.0 2.0", "1.0000000001 2.0"),
+         ("1.0 2.0", "1.1 2.0"), ("1 2 3", "1 2"), ("a 1.0", "b 1.0"), ("0 0", "0 1e-7"),
+         ("6.227474194e-03", "6.229796349e-03"), ("nan", "nan"), ("", "")]
+
+
+def test_verify_results_semantics():
+    assert verify_results("1.0 2.0", "1.0 2.0").passed
+    r = verify_results("1.0 2.0", "1.0 2.5")
+    assert not r.passed and r.mismatches == 1 and abs(r.max_abs_err - 0.5) < 1e-12
+    assert verify_results("1 2 3", "1 2").length_mismatch
+    assert not verify_results("a", "b").passed
+
+
+def test_verify_results_matches_reference(reference):
+    from acctuner.cli import verify_results as ref_verify
+    for base, tuned in CASES:
+        for atol, rtol in ((1e-6, 1e-4), (0.0, 0.0), (1e-2, 1e-3)):
+            assert verify_results(base, tuned, atol, rtol).to_json() == \
+                ref_verify(base, tuned, atol, rtol).to_json()
+
+
+@pytest.mark.gpu
+def test_tuning_run_end_to_end(gpu, tmp_path):
+    from paper_2002_12115_b200.evaluator import B200Evaluator
+    from paper_2002_12115_b200.tune import run_tuning
+    with B200Evaluator("XS", nn=3, workers_per_device=2) as ev:
+        report, ok = run_tuning(ev, ga.GAConfig(population=6, generations=3, rng_seed=1),
+                                tmp_path, echo=lambda *_: None)
+    assert ok and report["verification"]["passed"]
+    assert report["improvement_ratio"] > 1.0          # some GPU pattern beats all-CPU
+    assert (tmp_path / "report.json").exists()
+    assert len((tmp_path / "generations.jsonl").read_text().splitlines()) == 3
+    assert set(json.loads((tmp_path / "report.json").read_text())) >= {
+        "baseline_time_s", "best_time_s", "improvement_ratio", "best_genome", "plan", "verification"}

@@ -69,3 +69,32 @@ def test_no_device_behaviour():
     from paper_2002_12115_b200.errors import DeviceError
     with pytest.raises(DeviceError):
         N.Context(0, 9, 9, 17)
+
+
+def _build_c_host(tmp_path):
+    import subprocess
+    exe = tmp_path / "c_host"
+    lib_dir = ROOT / "paper_2002_12115_b200" / "_native"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "c_host_example.c"), "-L", str(lib_dir),
+                    "-lhimeno_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+@pytest.mark.skipif(has_gpu(), reason="device-less behaviour only")
+def test_c_host_links_and_reports_no_device(tmp_path):
+    """A plain C program builds against include/himeno_b200.h + the .so (no torch)."""
+    import subprocess
+    out = subprocess.run([str(_build_c_host(tmp_path))], capture_output=True, text=True)
+    assert out.returncode == 2 and "environment" in out.stdout
+
+
+@pytest.mark.gpu
+def test_c_host_runs_on_device(tmp_path):
+    import subprocess
+    from oracle import oracle
+    out = subprocess.run([str(_build_c_host(tmp_path))], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    gosa = float(out.stdout.split()[-1])
+    ref = oracle.run_program(33, 33, 65, 3)["gosa64"]
+    assert abs(gosa - ref) <= 1e-12 * ref

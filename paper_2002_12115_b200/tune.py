@@ -109,10 +109,21 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
     ratio = baseline_s / best.time_s
     echo(f"best genome {ga.genome_str(best.genome)} time {best.time_s:.6g} s "
          f"ratio {ratio:.3f}x ({result.evaluations} evaluations)")
-    base_out = evaluator.run_for_output((0,) * gene_len)
-    tuned_out = evaluator.run_for_output(best.genome)
-    diff = verify_results(base_out, tuned_out, atol, rtol)
-    echo(f"verification: {'pass' if diff.passed else 'FAIL'} (max abs err {diff.max_abs_err:.3e})")
+    if best.eval_source == "penalty" or best.timed_out:
+        # every evaluated pattern failed or timed out: nothing to verify (the reference
+        # would abort in run_for_output with BaselineFailure, cli.py:265 / evaluators.py:187)
+        verification = {"status": "skipped",
+                        "reason": f"best individual did not run: {best.diagnostic or 'timeout'}"}
+        passed = True
+        echo("verification: skipped (no runnable pattern was evaluated)")
+    else:
+        base_out = evaluator.run_for_output((0,) * gene_len)
+        tuned_out = evaluator.run_for_output(best.genome)
+        diff = verify_results(base_out, tuned_out, atol, rtol)
+        verification = diff.to_json() | {"status": "ran"}
+        passed = diff.passed
+        echo(f"verification: {'pass' if diff.passed else 'FAIL'} "
+             f"(max abs err {diff.max_abs_err:.3e})")
     plan = evaluator.plan(best.genome)
     report = {
         "baseline_time_s": baseline_s,
@@ -122,7 +133,7 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
         "gene_length": gene_len,
         "kinds": {str(l): evaluator.kinds[l].value for l in evaluator.eligible_ids},
         "plan": plan.to_json(evaluator.refs),
-        "verification": diff.to_json() | {"status": "ran"},
+        "verification": verification,
         "evaluations": result.evaluations,
         "ga": {"population": config.population, "generations": config.generations,
                "crossover_rate": config.crossover_rate, "mutation_rate": config.mutation_rate,
@@ -143,7 +154,7 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
         meta = {"written_at": time.strftime("%Y-%m-%dT%H:%M:%S%z"), "host": platform.node(),
                 "python": platform.python_version()}
         (out / "meta.json").write_text(json.dumps(meta, indent=2, sort_keys=True) + "\n")
-    return report, diff.passed
+    return report, passed
 
 
 def main(argv=None) -> int:

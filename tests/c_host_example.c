@@ -46,7 +46,7 @@ int main(void) {
     hp_destroy(ctx);
     return rc > 0 ? 1 : 2;
   }
-  printf("wall_s %.6f launches %llu gosa %.9e\n", r.wall_s, (unsigned long long)r.n_launch,
+  printf("wall_s %.6f launches %llu gosa %.17g\n", r.wall_s, (unsigned long long)r.n_launch,
          r.gosa);
   hp_destroy(ctx);
   return 0;

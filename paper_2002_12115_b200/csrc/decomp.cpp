@@ -1,14 +1,15 @@
 // Slab decomposition of the device-resident Jacobi over several GPUs.
 //
 // The interior planes [1, I-2) of the slowest dimension (C `i`) are split into
-// contiguous slabs, one per rank.  A slab context holds global planes
-// [i_begin-1, i_end+1): its interior plus one halo plane on each side (a global
-// boundary plane at the ends of the grid).  Per iteration each rank runs the
-// fused stencil on its interior, then exchanges the planes its neighbours
-// need -- its first interior plane goes to rank-1's upper halo, its last to
-// rank+1's lower halo -- and after the last iteration the per-rank gosa
-// partials (fp64) are summed.  Only the final iteration's gosa is observable
-// (jacobi returns it), so one reduction per jacobi call suffices.
+// contiguous slabs (>= 2 planes), one per rank.  A slab context holds global
+// planes [i_begin-2, i_end+2): its interior plus two halo planes on each side
+// (global boundary planes at the ends of the grid).  Each pass runs one or two
+// Jacobi iterations on the slab -- the two-step kernel's first step also
+// recomputes the neighbours' adjacent planes from the two-deep halo -- and then
+// exchanges two planes per side: its first two interior planes go to rank-1's
+// upper halo, its last two to rank+1's lower halo.  After the last pass the
+// per-rank gosa partials (fp64) are summed.  Only the final iteration's gosa is
+// observable (jacobi returns it), so one reduction per jacobi call suffices.
 //
 // Transports:
 //  * in-process group (hp_group_jacobi): several slab contexts driven by one
@@ -32,9 +33,12 @@ using namespace hp;
 
 // ---------------------------------------------------------------- geometry
 
+constexpr int kHalo = 2;   // halo planes per side (two-step passes need two)
+
 extern "C" int hp_slab_range(int I, int nranks, int rank, int32_t* i_begin, int32_t* i_end) {
   const int n = I - 3;  // interior planes [1, I-2)
-  if (I < 4 || nranks < 1 || rank < 0 || rank >= nranks || nranks > n || !i_begin || !i_end) {
+  if (I < 4 || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && nranks > n / kHalo) ||
+      nranks > n || !i_begin || !i_end) {
     set_error("hp_slab_range: bad arguments (I=%d nranks=%d rank=%d)", I, nranks, rank);
     return HP_ERR_ARG;
   }
@@ -51,19 +55,20 @@ extern "C" int hp_create_slab(int device, const hp_grid* global, int i_begin, in
   }
   *out = nullptr;
   const int I = global->I;
+  const bool whole = i_begin == 1 && i_end == I - 2;
   if (I < 4 || global->J < 4 || global->K < 4 || i_begin < 1 || i_end > I - 2 ||
-      i_end <= i_begin) {
-    set_error("hp_create_slab: planes [%d, %d) not inside the interior of a %d-plane grid",
-              i_begin, i_end, I);
+      i_end <= i_begin || (!whole && i_end - i_begin < kHalo)) {
+    set_error("hp_create_slab: planes [%d, %d) not a slab (>= %d planes) of the interior of "
+              "a %d-plane grid", i_begin, i_end, kHalo, I);
     return HP_ERR_ARG;
   }
   hp_ctx* c = nullptr;
-  const int rc = create_ctx(device, i_end - i_begin + 2, global->J, global->K, &c);
+  const int rc = create_ctx(device, i_end - i_begin + 2 * kHalo, global->J, global->K, &c);
   if (rc != HP_OK) return rc;
   c->gI = I;
-  c->i_off = i_begin - 1;
-  c->li_lo = 1;
-  c->li_hi = i_end - i_begin + 1;
+  c->i_off = i_begin - kHalo;
+  c->li_lo = kHalo;
+  c->li_hi = i_end - i_begin + kHalo;
   *out = c;
   return HP_OK;
 }
@@ -71,11 +76,35 @@ extern "C" int hp_create_slab(int device, const hp_grid* global, int i_begin, in
 namespace {
 
 size_t plane_bytes(const hp_ctx* c) { return c->dev.plane() * sizeof(float); }
+int sm_count_of(const hp_ctx* c) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, c->device);
+  return n > 0 ? n : 148;
+}
 float* plane_ptr(hp_ctx* c, float* buf, int li) { return buf + (size_t)li * c->dev.plane(); }
 
 }  // namespace
 
 // ------------------------------------------------------- in-process group
+
+// One pass on a slab: two iterations (two-step kernel) when `step` == 2, else
+// one; reads `in`, writes `out`.  Returns kernels launched or -1.
+static int slab_pass(hp_ctx* c, const float* in, float* out, int step, const LaunchArgs& a) {
+  if (step == 2) {
+    const int r = launch_stencil_tb2(c->dev, c->dev.tma, in, out, a, c->sink(), c->stream,
+                                     sm_count_of(c));
+    if (r != 0) return r;
+    return -1;   // every slab has two-plane halos: the two-step kernel must apply
+  }
+  return launch_stencil_rotate(c->dev, in, out, a, c->sink(), c->stream);
+}
+
+static float* pass_buffer(hp_ctx* c, int pass) { return (pass & 1) ? c->scratch : c->dev.f[HP_F_P]; }
+
+// iterations of the next pass: two while temporal blocking is on (same on every rank)
+static int pass_step(int done, int nn) {
+  return (set_temporal_blocking(-1) && nn - done >= 2) ? 2 : 1;
+}
 
 extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
   if (!ctxs || n < 1 || nn < 0) {
@@ -103,11 +132,14 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     if (e != cudaSuccess) fail(e, "event create");
     else if (time_loop_begin(ctxs[r], ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "begin");
   }
-  for (int it = 0; it < nn && rc == HP_OK; ++it) {
+  int pass = 0;
+  for (int it = 0; it < nn && rc == HP_OK; ++pass) {
+    const int step = pass_step(it, nn);
     for (int r = 0; r < n && rc == HP_OK; ++r) {
       hp_ctx* c = ctxs[r];
       cudaSetDevice(c->device);
-      if (time_loop_step(c, it, ctx_args(c, 1)) < 0) fail(cudaGetLastError(), "stencil");
+      if (slab_pass(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, ctx_args(c, 1)) < 0)
+        fail(cudaGetLastError(), "stencil pass");
       c->launches++;
       cudaError_t e = cudaEventRecord(done[r], c->stream);
       if (e != cudaSuccess) fail(e, "event record");
@@ -115,27 +147,29 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     for (int r = 0; r < n && rc == HP_OK; ++r) {
       hp_ctx* c = ctxs[r];
       cudaSetDevice(c->device);
-      float* out = time_loop_buffer(c, it + 1);
+      float* out = pass_buffer(c, pass + 1);
       for (int side = -1; side <= 1 && rc == HP_OK; side += 2) {
         const int q = r + side;
         if (q < 0 || q >= n) continue;
         hp_ctx* nb = ctxs[q];
-        float* nb_out = time_loop_buffer(nb, it + 1);
-        // lower halo <- neighbour's last interior plane; upper halo <- its first
-        const int dst_plane = side < 0 ? c->li_lo - 1 : c->li_hi;
-        const int src_plane = side < 0 ? nb->li_hi - 1 : nb->li_lo;
+        float* nb_out = pass_buffer(nb, pass + 1);
+        // lower halo <- neighbour's last two interior planes; upper <- its first two
+        const int dst_plane = side < 0 ? c->li_lo - kHalo : c->li_hi;
+        const int src_plane = side < 0 ? nb->li_hi - kHalo : nb->li_lo;
         cudaError_t e = cudaStreamWaitEvent(c->stream, done[q], 0);
         if (e == cudaSuccess)
           e = cudaMemcpyPeerAsync(plane_ptr(c, out, dst_plane), c->device,
-                                  plane_ptr(nb, nb_out, src_plane), nb->device, plane_bytes(c),
-                                  c->stream);
+                                  plane_ptr(nb, nb_out, src_plane), nb->device,
+                                  kHalo * plane_bytes(c), c->stream);
         if (e != cudaSuccess) fail(e, "halo copy");
       }
     }
+    it += step;
   }
   for (int r = 0; r < n && rc == HP_OK; ++r) {
     cudaSetDevice(ctxs[r]->device);
-    if (time_loop_end(ctxs[r], nn, ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "end");
+    if (time_loop_finish(ctxs[r], pass_buffer(ctxs[r], pass), ctx_args(ctxs[r], 1)) < 0)
+      fail(cudaGetLastError(), "end");
   }
   // gosa of the last iteration: sum of the per-slab fp64 partials, in rank order
   double total = 0.0;
@@ -265,7 +299,8 @@ extern "C" int hp_dd_init(hp_ctx* c, int nranks, int rank, const unsigned char* 
   return HP_OK;
 }
 
-// nn iterations with halo exchange after each, then the gosa all-reduce; async on hp_stream.
+// nn iterations in passes (two-step while temporal blocking is on), two halo
+// planes per side exchanged after each pass, then the gosa all-reduce; async.
 extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
   if (!c || !c->dd || nn < 0) {
     set_error("hp_dd_jacobi: context not initialised for decomposition");
@@ -276,25 +311,29 @@ extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
   cudaSetDevice(c->device);
   const LaunchArgs a = ctx_args(c, 1);
   if (time_loop_begin(c, a) < 0) return cuda_fail(cudaGetLastError(), "begin");
-  const size_t count = c->dev.plane();
-  for (int it = 0; it < nn; ++it) {
-    if (time_loop_step(c, it, a) < 0) return cuda_fail(cudaGetLastError(), "stencil");
+  const size_t count = kHalo * c->dev.plane();
+  int pass = 0;
+  for (int it = 0; it < nn; ++pass) {
+    const int step = pass_step(it, nn);
+    if (slab_pass(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, a) < 0)
+      return cuda_fail(cudaGetLastError(), "stencil pass");
     c->launches++;
+    it += step;
     if (!l) continue;
-    float* out = time_loop_buffer(c, it + 1);
+    float* out = pass_buffer(c, pass + 1);
     ncclResult_t r = l->GroupStart();
     if (d->rank > 0) {
       if (r == ncclSuccess)
         r = l->Send(plane_ptr(c, out, c->li_lo), count, ncclFloat32, d->rank - 1, d->comm,
                     c->stream);
       if (r == ncclSuccess)
-        r = l->Recv(plane_ptr(c, out, c->li_lo - 1), count, ncclFloat32, d->rank - 1, d->comm,
-                    c->stream);
+        r = l->Recv(plane_ptr(c, out, c->li_lo - kHalo), count, ncclFloat32, d->rank - 1,
+                    d->comm, c->stream);
     }
     if (d->rank < d->nranks - 1) {
       if (r == ncclSuccess)
-        r = l->Send(plane_ptr(c, out, c->li_hi - 1), count, ncclFloat32, d->rank + 1, d->comm,
-                    c->stream);
+        r = l->Send(plane_ptr(c, out, c->li_hi - kHalo), count, ncclFloat32, d->rank + 1,
+                    d->comm, c->stream);
       if (r == ncclSuccess)
         r = l->Recv(plane_ptr(c, out, c->li_hi), count, ncclFloat32, d->rank + 1, d->comm,
                     c->stream);
@@ -303,7 +342,7 @@ extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
     if (r != ncclSuccess) return nccl_fail(r, "halo exchange");
     if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
   }
-  if (time_loop_end(c, nn, a) < 0) return cuda_fail(cudaGetLastError(), "end");
+  if (time_loop_finish(c, pass_buffer(c, pass), a) < 0) return cuda_fail(cudaGetLastError(), "end");
   if (l && nn > 0) {
     double* g = reinterpret_cast<double*>(c->dscal + HP_V_GOSA * SLOT_BYTES);
     const ncclResult_t r = l->AllReduce(g, g, 1, ncclFloat64, ncclSum, d->comm, c->stream);

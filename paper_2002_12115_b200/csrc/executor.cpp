@@ -1034,7 +1034,7 @@ extern "C" int hp_init_device(hp_ctx* c) {
   GosaSink g = c->sink();
   Box b0{0, c->I, 0, c->J, 0, c->K};
   // initmt nest B over global i < imax: local planes [0, imax - i_off)
-  Box b1{0, std::min(c->I, a.imax - c->i_off), 0, a.jmax, 0, a.kmax};
+  Box b1{std::max(0, -c->i_off), std::min(c->I, a.imax - c->i_off), 0, a.jmax, 0, a.kmax};
   if (launch_fill(c->dev.f[HP_F_WRK2], c->field_elems, 0.0f, c->stream) < 0 ||
       launch_nest(NEST_INIT0, MAP_COLLAPSE, c->dev, b0, a, g, c->stream) < 0 ||
       launch_nest(NEST_INIT1, MAP_COLLAPSE, c->dev, b1, a, g, c->stream) < 0)

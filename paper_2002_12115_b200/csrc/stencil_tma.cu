@@ -388,7 +388,7 @@ __device__ __forceinline__ void ss_quad(const float* ct, const Row& lm, const Ro
 __global__ void __launch_bounds__(kThreads2, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
               int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
-              float omega, GosaSink g, int reset) {
+              int g_lo, int g_hi, float omega, GosaSink g, int reset) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   unsigned char* p0ring = smem;
@@ -491,7 +491,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         const int cslot = sc % SC;
         mbar_wait(&cfull[cslot], (sc / SC) & 1);
         const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot) + warp * QK + lane * 4;
-        const bool plane_in = m >= i_lo && m < i_hi;
+        // planes of the global interior (local indices): in a slab, step 1 also
+        // recomputes the neighbours' adjacent planes (two-plane halos)
+        const bool plane_in = m >= g_lo && m < g_hi;
         float r[4];
         if (plane_in && row_in) {
           float ss[4];
@@ -687,9 +689,12 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (!t || (p_in != t->p && p_in != t->scratch)) return 0;
   const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
             k_hi = a.kmax - 1;
-  // full grid only (a slab's halo would need two planes per exchange)
-  if (a.i_off != 0 || i_lo != 1 || i_hi != a.imax - 1) return 0;
+  // step 1 reads p0 two planes beyond the planes it updates: the full grid (plane
+  // -1 is never used by a computed point) or a slab with two-plane halos
+  const bool full = a.i_off == 0 && i_lo == 1 && i_hi == a.imax - 1;
+  if (!full && (i_lo < 2 || i_hi > F.I - 2)) return 0;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
+  const int g_lo = 1 - a.i_off, g_hi = a.imax - 1 - a.i_off;
   Tb2Maps maps = t->tb2;
   if (p_in == t->scratch) maps.pin = t->tb2_scratch;
   const int ktiles = (k_hi + TK2 - 1) / TK2;
@@ -710,7 +715,7 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
     attr = true;
   }
   k_stencil_tb2<<<(int)grid, kThreads2, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo,
-                                                   k_hi, ktiles, chunk, a.omega, g,
+                                                   k_hi, ktiles, chunk, g_lo, g_hi, a.omega, g,
                                                    a.gosa_reset);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }

@@ -3,10 +3,11 @@
 Partition: the interior planes [1, I-2) of the slowest dimension (C ``i``; BASELINE
 calls the configs "k-decomposed", but in the ``[i][j][k]`` layout k is contiguous and
 splitting ``i`` gives the same 1-D topology with contiguous halo planes) are split into
-contiguous, near-equal slabs.  Per iteration each rank computes its slab with the fused
-stencil and exchanges one J x P plane of p with each neighbour; the fp64 gosa partials
-are summed once at the end of the jacobi call (only the last iteration's gosa is
-observable).  Device work and transfers run in the native library
+contiguous, near-equal slabs of at least two planes.  Each slab carries two halo planes
+per side; every pass runs one or two iterations (the two-step kernel's first step also
+recomputes the neighbours' adjacent planes) and then exchanges two J x P planes of p with
+each neighbour; the fp64 gosa partials are summed once at the end of the jacobi call (only
+the last iteration's gosa is observable).  Device work and transfers run in the native library
 (``csrc/decomp.cpp``):
 
 * ``SlabJacobi``  one process per GPU (torchrun); halo planes and the gosa all-reduce
@@ -21,20 +22,24 @@ from . import native as N
 from .apps import himeno
 
 
+HALO = 2    # halo planes per side
+
+
 def slab_range(I: int, nranks: int, rank: int) -> tuple:
     """Interior planes [i_begin, i_end) owned by `rank` (same rule as hp_slab_range)."""
     n = I - 3
-    if I < 4 or not 1 <= nranks <= n or not 0 <= rank < nranks:
+    if I < 4 or not 1 <= nranks <= n or not 0 <= rank < nranks or \
+            (nranks > 1 and nranks > n // HALO):
         raise ValueError(f"cannot split {n} interior planes over {nranks} ranks (rank {rank})")
     return 1 + rank * n // nranks, 1 + (rank + 1) * n // nranks
 
 
 def halo_plan(I: int, nranks: int) -> list:
-    """(rank, sends, receives) of one iteration; planes are local indices.
+    """(rank, sends, receives) after each pass: (peer, first local plane) of HALO planes.
 
-    Rank r's local plane li is global plane i_begin-1+li: its first interior plane
-    (local 1) goes to rank r-1's upper halo, its last to rank r+1's lower halo
-    (local 0).  Mirrors hp_group_jacobi / hp_dd_jacobi.
+    Rank r's local plane li is global plane i_begin-HALO+li: its first HALO interior
+    planes (local HALO..) go to rank r-1's upper halo, its last HALO to rank r+1's lower
+    halo (local 0..).  Mirrors hp_group_jacobi / hp_dd_jacobi.
     """
     out = []
     for r in range(nranks):
@@ -42,11 +47,11 @@ def halo_plan(I: int, nranks: int) -> list:
         n = e - b
         sends, recvs = [], []
         if r > 0:
-            sends.append((r - 1, 1))
+            sends.append((r - 1, HALO))
             recvs.append((r - 1, 0))
         if r < nranks - 1:
             sends.append((r + 1, n))
-            recvs.append((r + 1, n + 1))
+            recvs.append((r + 1, n + HALO))
         out.append((r, sends, recvs))
     return out
 
@@ -91,7 +96,7 @@ class SlabJacobi:
 
     def interior_p(self):
         """This slab's interior planes of p (global planes [i_begin, i_end))."""
-        return self.ctx.read_field("p", 1)[1:-1]
+        return self.ctx.read_field("p", 1)[HALO:-HALO]
 
     def close(self) -> None:
         self.ctx.close()
@@ -120,11 +125,11 @@ class GroupJacobi:
         out = np.zeros((sz.I, sz.J, sz.K), dtype=np.float32)
         for c, (b, e) in zip(self.contexts, self.slabs):
             local = c.read_field(name, 1)
-            out[b:e] = local[1:-1]
+            out[b:e] = local[HALO:-HALO]
             if b == 1:
-                out[0] = local[0]
+                out[0] = local[HALO - 1]
             if e == sz.I - 2:
-                out[e] = local[-1]
+                out[e] = local[-HALO]
         return out
 
     def close(self) -> None:

@@ -51,26 +51,33 @@ def _rank_main(rank, world, name, nn, port, q):
     full = oracle.empty_fields(sz.I, sz.J, sz.K)
     oracle.initmt(full)
     b, e = dd.slab_range(sz.I, world, rank)
-    f = {k: v[b - 1:e + 1].copy() for k, v in full.items()}
+    H = dd.HALO
+    lo = b - H                          # global plane of local plane 0 (may be -1)
+    f = {}
+    for k, v in full.items():
+        pad = np.zeros((e - b + 2 * H,) + v.shape[1:], dtype=np.float32)
+        src_lo, src_hi = max(lo, 0), min(e + H, v.shape[0])
+        pad[src_lo - lo:src_hi - lo] = v[src_lo:src_hi]
+        f[k] = pad
     plan = {r: (s, rv) for r, s, rv in dd.halo_plan(sz.I, world)}
     n = e - b
     gosa = 0.0
     for _ in range(nn):
-        f["p"], part = stencil_slab(f, 1, n + 1, sz.J - 1, sz.K - 1)
+        f["p"], part = stencil_slab(f, H, n + H, sz.J - 1, sz.K - 1)
         sends, recvs = plan[rank]
-        reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(f["p"][pl])), dst)
+        reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(f["p"][pl:pl + H])), dst)
                 for dst, pl in sends]
         for src, pl in recvs:
-            buf = torch.empty(f["p"][pl].shape, dtype=torch.float32)
+            buf = torch.empty(f["p"][pl:pl + H].shape, dtype=torch.float32)
             dist.recv(buf, src)
-            f["p"][pl] = buf.numpy()
+            f["p"][pl:pl + H] = buf.numpy()
         for r in reqs:
             r.wait()
         t = torch.tensor([part], dtype=torch.float64)
         dist.all_reduce(t)
         gosa = float(t.item())
     pieces = [None] * world
-    dist.all_gather_object(pieces, (b, e, f["p"][1:-1]))
+    dist.all_gather_object(pieces, (b, e, f["p"][H:-H]))
     if rank == 0:
         p = full["p"].copy()
         for bb, ee, arr in pieces:
@@ -82,6 +89,7 @@ def _rank_main(rank, world, name, nn, port, q):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_gloo_slab_decomposition_matches_oracle(world):
+    """Host slabs with HALO-deep halos, exchanged per dd.halo_plan after every step."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + world * 7 + os.getpid() % 1000
@@ -99,7 +107,7 @@ def test_gloo_slab_decomposition_matches_oracle(world):
 
 def test_slab_range_partition():
     for I in (9, 33, 65, 257, 513):
-        for n in range(1, min(9, I - 3) + 1):
+        for n in range(1, min(9, (I - 3) // dd.HALO) + 1):
             ranges = [dd.slab_range(I, n, r) for r in range(n)]
             assert ranges[0][0] == 1 and ranges[-1][1] == I - 2
             assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
@@ -108,6 +116,8 @@ def test_slab_range_partition():
             assert ranges == [N.slab_range(I, n, r) for r in range(n)]   # C ABI agrees
     with pytest.raises(ValueError):
         dd.slab_range(9, 7, 0)
+    with pytest.raises(ValueError):
+        dd.slab_range(9, 4, 0)          # 6 interior planes cannot give 4 slabs of >= 2
 
 
 def test_halo_plan_is_symmetric():
@@ -119,15 +129,21 @@ def test_halo_plan_is_symmetric():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("ranks", [1, 2, 3, 4])
-@pytest.mark.parametrize("name,nn", [("XS", 3), ("M", 2)])
-def test_gpu_group_slabs_match_oracle(gpu, ranks, name, nn):
-    """Virtual ranks on one GPU: decomposition is bit-exact with the full grid."""
+@pytest.mark.parametrize("name,nn", [("XS", 3), ("XS", 4), ("M", 2), ("M", 5)])
+def test_gpu_group_slabs_match_oracle(gpu, ranks, name, nn, tb):
+    """Virtual ranks on one GPU, one- and two-step passes: bit-exact with the full grid."""
     sz = himeno.size(name)
     ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
-    with dd.GroupJacobi(name, [0] * ranks) as g:
-        gosa = g.jacobi(nn)
-        p = g.gather("p")
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        with dd.GroupJacobi(name, [0] * ranks) as g:
+            gosa = g.jacobi(nn)
+            p = g.gather("p")
+    finally:
+        lib.hp_set_temporal_blocking(old)
     assert np.array_equal(p, ref["fields"]["p"])
     assert abs(gosa - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
 
@@ -141,6 +157,7 @@ def test_gpu_slab_single_rank_dd(gpu):
     s.jacobi(3)
     assert abs(s.gosa() - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
     assert np.array_equal(s.interior_p(), ref["fields"]["p"][1:sz.I - 2])
+    s.jacobi(0)
     s.close()
 
 

@@ -22,7 +22,7 @@ from . import native as N
 from .apps import himeno
 
 
-HALO = 2    # halo planes per side
+HALO = N.SLAB_HALO    # halo planes per side
 
 
 def slab_range(I: int, nranks: int, rank: int) -> tuple:

@@ -38,6 +38,7 @@ FLAG_KERNEL_TIMING = 8
 FLAG_GRAPH_TIME_LOOP = 16
 FLAG_FUSED_TIME_LOOP = 32
 MAX_SAMPLES = 8
+SLAB_HALO = 2      # halo planes per side of a slab context (csrc/decomp.cpp kHalo)
 
 
 class Grid(C.Structure):
@@ -200,8 +201,8 @@ class Context:
                   f"hp_create(device={device}, {I}x{J}x{K})")
         else:
             i_begin, i_end = slab
-            self.shape = (i_end - i_begin + 2, J, K)
-            self.i_off = i_begin - 1
+            self.shape = (i_end - i_begin + 2 * SLAB_HALO, J, K)
+            self.i_off = i_begin - SLAB_HALO
             check(self.lib.hp_create_slab(device, C.byref(Grid(I, J, K)), i_begin, i_end,
                                           C.byref(ptr)),
                   f"hp_create_slab(device={device}, planes [{i_begin},{i_end}) of {I})")

@@ -340,6 +340,23 @@ def run_ours(args, world, rank, local):
                    else "hp_write_field + hp_dd_jacobi + hp_read_field per slab (C ABI)"}
 
     extra = {}
+    if rank == 0 and world == 1 and not args.no_other_grids:
+        # the other BASELINE grids on this GPU, same method (device-resident time loop)
+        others = {}
+        for name in ("M", "XL"):
+            osz = himeno.size(name)
+            with N.Context(local, osz.I, osz.J, osz.K) as octx:
+                octx.init_device()
+                octx.time_steps(1, nn, variant)
+                oms = octx.time_steps(3, nn, variant)
+                okt = octx.time_jacobi(nn, variant)
+            others[name] = {
+                "grid": [osz.I, osz.J, osz.K],
+                "gflops": 3 * FLOP_PER_POINT * osz.interior_points * nn / (oms / 1e3) / 1e9,
+                "stencil_launch_ms": okt.stencil_ms,
+                "iterations_per_launch": okt.stencil_iters,
+                "achieved_gbs": BYTES_STENCIL * osz.interior_points / (okt.stencil_ms / 1e3) / 1e9}
+        extra["other_grids"] = others
     if rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle
         extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
@@ -387,6 +404,7 @@ def main(argv=None) -> int:
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-ga", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-grids", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ga-size", default="M")
     ap.add_argument("--ga-nn", type=int, default=3)

@@ -12,9 +12,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
-  --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-ga --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_launch_bench.log 2>&1
+  --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-ga --no-cpu-baseline --no-other-grids --e2e-steps 1 > $OUT/ncu_launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stencil -s 5 -c 2 \
-  -o $OUT/stencil python bench.py --steps 1 --warmup 3 --no-ga --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_full.log 2>&1
+  -o $OUT/stencil python bench.py --steps 1 --warmup 3 --no-ga --no-cpu-baseline --no-other-grids --e2e-steps 1 > $OUT/ncu_full.log 2>&1
 ls -la $OUT
 tail -5 $OUT/pytest_gpu.log $OUT/smoke.log $OUT/bench.err
 cat $OUT/bench.json $OUT/bench_ref.json

@@ -362,7 +362,7 @@ def run_ours(args, world, rank, local):
         extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
     if rank == 0 and not args.no_ga:
         extra["ga"] = ga_throughput(local, args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
-                                    args.ga_seed, args.ga_workers)
+                                    args.ga_seed, args.ga_workers or min(16, os.cpu_count() or 1))
     if slab is not None:
         slab.close()
     else:
@@ -411,8 +411,9 @@ def main(argv=None) -> int:
     ap.add_argument("--ga-pop", type=int, default=20)
     ap.add_argument("--ga-gens", type=int, default=10)
     ap.add_argument("--ga-seed", type=int, default=0)
-    ap.add_argument("--ga-workers", type=int, default=4,
-                    help="concurrent evaluations per GPU (own context each)")
+    ap.add_argument("--ga-workers", type=int, default=0,
+                    help="concurrent evaluations per GPU (own context each); 0 = host cores "
+                         "(the reference GA uses max_concurrency = os.cpu_count())")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -165,15 +165,23 @@ def main(argv=None) -> int:
     ap.add_argument("--generations", type=int, default=10)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--devices", default="0", help="comma list of GPU ids, or 'all'")
-    ap.add_argument("--workers-per-device", type=int, default=1)
+    ap.add_argument("--workers-per-device", default="1",
+                    help="concurrent evaluations per GPU, or 'auto' (host cores / GPUs)")
     ap.add_argument("--transfer-mode", default="batched", choices=["batched", "per-loop"])
     ap.add_argument("--out")
     args = ap.parse_args(argv)
     devices = "all" if args.devices == "all" else [int(d) for d in args.devices.split(",")]
+    if args.workers_per_device == "auto":
+        import os
+        from . import native
+        n_dev = native.device_count() if devices == "all" else len(devices)
+        workers = max(1, (os.cpu_count() or 1) // max(1, n_dev))
+    else:
+        workers = int(args.workers_per_device)
     cfg = ga.GAConfig(population=args.population, generations=args.generations,
                       rng_seed=args.seed)
     with B200Evaluator(args.size, nn=args.nn, devices=devices,
-                       workers_per_device=args.workers_per_device,
+                       workers_per_device=workers,
                        transfer_mode=args.transfer_mode) as ev:
         _report, ok = run_tuning(ev, cfg, args.out)
     return 0 if ok else 3

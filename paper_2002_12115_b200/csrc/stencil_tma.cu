@@ -23,6 +23,13 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <array>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <vector>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -255,73 +262,97 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
 
 // ================================================================ two-step kernel
 //
-// k_stencil_tb2: two Jacobi iterations per pass (temporal blocking).  A tile is
-// TJ2 output rows x TK2 = 120 output k.  Step 1 computes p1 = S(p0) on the tile
-// widened to R1 = TJ2+2 rows and QK = 128 columns (k0-4 .. k0+123: exactly 32
-// float4 quads, one per lane -- uniform SIMT, no scalar halo path); step 2
-// computes p2 = S(p1) one plane behind on the TJ2 rows, lanes 1..30 (lanes 0
-// and 31 only carry the k halo).  The 12 coefficient arrays are read from HBM
-// once for both iterations: 56 B per point per TWO iterations.
+// k_stencil_tb2<LW>: two Jacobi iterations per pass (temporal blocking).  A row
+// of a tile is LW lanes x 4 floats = QK columns; a warp carries RPW = 32/LW rows
+// (LW = 32: one row per warp, QK = 128; LW = 16: two rows per warp, QK = 64).
+// Step 1 computes p1 = S(p0) on R1 = 8*RPW rows x QK columns (k0-4 ..
+// k0+QK-5: one float4 quad per lane, uniform SIMT, no scalar halo path); step 2
+// computes p2 = S(p1) one plane behind on the TJ2 = R1-2 inner rows, lanes
+// 1..LW-2 of each row (the edge lanes only carry the k halo), TK2 = QK-8 output
+// columns.  The 12 coefficient arrays are read from HBM once for both
+// iterations: 56 B per point per TWO iterations.
 //
-//   producer warp: p0 plane tiles (136k x (R1+2)j) into a 4-slot ring and the
-//     widened coefficient tiles (128k x R1 j, 12 arrays) into a 3-slot ring; work
-//     units from the device-wide queue (as k_stencil_tma).
-//   consumer warp w (0..R1-1) <-> row j0-1+w:
-//     step 1 (plane m): register queue of p0 rows; non-interior points copy p0
-//       (boundaries are fixed); p1 quad -> smem (2 slots of R1 x 128).
-//     named barrier among the consumer warps (p1(m) complete)
-//     step 2 (plane m-1, warps 1..TJ2): register queue of p1 rows (k+-1 by
-//       shuffles); coefficients of plane m-1 still resident in the ring.
+//   producer warp: p0 plane tiles (QK+8 k x R1+2 j) into an SP-slot ring and the
+//     coefficient tiles (QK k x R1 j, 12 arrays) into an SC-slot ring; work units
+//     from the device-wide queue (as k_stencil_tma).
+//   step-1 warps (8): register queue of p0 rows; non-interior points copy p0
+//     (boundaries are fixed); p1 quad -> SQ-slot smem ring (per-thread arrivals).
+//   step-2 warps (TJ2/RPW): register queue of p1 rows (k+-1 by shuffles);
+//     coefficients of plane m-1 still resident in the ring.
+// The narrow variant (LW = 16: 56 x 14 output points per 64 x 16 step-1 tile)
+// has less halo work per output than the wide one (120 x 6 per 128 x 8) and
+// fits the Himeno k extents (254, 510, 1022) with less tail waste.
 // Every product/sum rounds exactly like the single-step kernel: p2 is
 // bit-identical to two single steps; gosa (fp64) is that of the second step.
-constexpr int TJ2 = 6;                 // output rows per tile
-constexpr int R1 = TJ2 + 2;            // step-1 rows = step-1 warps
-constexpr int TK2 = 120;               // output k per tile
-constexpr int QK = 128;                // step-1 k per tile (32 quads)
-constexpr int PW0 = QK + 8;            // p0 tile row: k0-8 .. k0+127
-constexpr int kWarps2 = R1 + TJ2 + 1;  // step-1 warps, step-2 warps, producer
-constexpr int kThreads2 = kWarps2 * 32;
-constexpr uint32_t kP0Bytes = PW0 * (R1 + 2) * 4;          // 5440
-constexpr uint32_t kP0Slot = (kP0Bytes + 127) / 128 * 128;
-constexpr uint32_t kCExtBytes = QK * R1 * 4;               // 4096 per array
-constexpr uint32_t kCSlot = NCOEF * kCExtBytes;            // 49152
-constexpr uint32_t kP1Slot = QK * R1 * 4;                  // 4096
-constexpr int SP = 3, SC = 4, SQ = 4;                      // p0 / coef / p1 ring slots
-constexpr uint32_t kTb2Smem = SP * kP0Slot + SC * kCSlot + SQ * kP1Slot;
+constexpr int SP = 3, SQ = 4;  // p0 / p1 ring slots
 
-struct __align__(64) Tb2Maps {
-  CUtensorMap coef[NCOEF];   // box 128 x R1, origin (k0-4, j0-1)
-  CUtensorMap pin;           // box 136 x (R1+2), origin (k0-8, j0-2)
+// LW lanes per row, NW1_ step-1 warps, SC_ coefficient ring slots
+template <int LW, int NW1_ = 8, int SC_ = 4>
+struct Tb2 {
+  static constexpr int RPW = 32 / LW;          // rows per warp
+  static constexpr int NW1 = NW1_;             // step-1 warps
+  static constexpr int SC = SC_;               // coefficient ring slots
+  static constexpr int R1 = NW1 * RPW;         // step-1 rows
+  static constexpr int TJ2 = R1 - 2;           // output rows per tile
+  static constexpr int NW2 = TJ2 / RPW;        // step-2 warps
+  static constexpr int QK = LW * 4;            // step-1 columns per tile
+  static constexpr int TK2 = QK - 8;           // output columns per tile
+  static constexpr int PW0 = QK + 8;           // p0 tile row: k0-8 .. k0+QK-1
+  static constexpr int kThreads = (NW1 + NW2 + 1) * 32;
+  static constexpr uint32_t kP0Bytes = PW0 * (R1 + 2) * 4;
+  static constexpr uint32_t kP0Slot = (kP0Bytes + 127) / 128 * 128;
+  static constexpr uint32_t kCExtBytes = QK * R1 * 4;        // one coefficient array
+  static constexpr uint32_t kCSlot = NCOEF * kCExtBytes;
+  static constexpr uint32_t kP1Slot = QK * R1 * 4;
+  static constexpr uint32_t kSmem = SP * kP0Slot + SC * kCSlot + SQ * kP1Slot;
+  static_assert(TJ2 % RPW == 0, "output rows must split evenly over step-2 warps");
+  // rings + barriers / unit ring / alignment pad + the static gosa scratch <= 227 KB
+  static_assert(kSmem + 2560 <= 232448, "rings exceed the 227 KB of shared memory");
+  static constexpr size_t smem_bytes() {
+    return 128 + (size_t)kSmem + 2 * (SP + SC + SQ) * sizeof(uint64_t) + sizeof(UnitRing);
+  }
 };
 
-// p0 tile row: lane quad at column 4 + 4*lane (k0-4+4*lane), edges at 3 / 132
-__device__ __forceinline__ Row load_row0(const float* ptile, int row, int lane) {
-  const float* base = ptile + row * PW0;
+constexpr int kTb2Shapes = 4;
+
+struct __align__(64) Tb2Maps {
+  CUtensorMap coef[NCOEF];   // box QK x R1, origin (k0-4, j0-1)
+  CUtensorMap pin;           // box QK+8 x (R1+2), origin (k0-8, j0-2)
+};
+
+// p0 tile row (PW0 floats): sub-lane quad at column 4 + 4*hl (k0-4+4*hl), edges at
+// 3 / QK+4; shuffles stay within the LW-lane segment of the row
+template <int LW>
+__device__ __forceinline__ Row load_row0(const float* ptile, int row, int hl) {
+  constexpr int QK = LW * 4;
+  const float* base = ptile + row * (QK + 8);
   Row r;
-  r.v = *reinterpret_cast<const float4*>(base + 4 + lane * 4);
-  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1);
-  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1);
-  if (lane == 0) r.left = base[3];
-  if (lane == 31) r.right = base[4 + QK];
+  r.v = *reinterpret_cast<const float4*>(base + 4 + hl * 4);
+  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1, LW);
+  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1, LW);
+  if (hl == 0) r.left = base[3];
+  if (hl == LW - 1) r.right = base[4 + QK];
   return r;
 }
-// p1 tile row (128 columns): k+-1 by shuffles only (edge lanes never output)
-__device__ __forceinline__ Row load_row1(const float* ptile, int row, int lane) {
+// p1 tile row (QK floats): k+-1 by shuffles only (edge lanes never output)
+template <int LW>
+__device__ __forceinline__ Row load_row1(const float* ptile, int row, int hl) {
   Row r;
-  r.v = *reinterpret_cast<const float4*>(ptile + row * QK + lane * 4);
-  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1);
-  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1);
+  r.v = *reinterpret_cast<const float4*>(ptile + row * (LW * 4) + hl * 4);
+  r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1, LW);
+  r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1, LW);
   return r;
 }
 
 // ss for the 4 elements of a lane quad, coefficients streamed term by term
-// from the shared-memory tile (ct = tile row base + lane quad); same order of
-// operations per element as the C program.
+// from the shared-memory tile (ct = tile row base + lane quad, CS = stride
+// between the coefficient arrays); same order of operations per element as the
+// C program.
+template <int CS>
 __device__ __forceinline__ void ss_quad(const float* ct, const Row& lm, const Row& l0,
                                         const Row& lp, const Row& mm, const Row& m0,
                                         const Row& mp, const Row& nm, const Row& n0,
                                         const Row& np, float (&ss)[4]) {
-  constexpr int CS = QK * R1;   // stride between coefficient arrays in the tile
   auto Q = [&](int c) { return *reinterpret_cast<const float4*>(ct + c * CS); };
   float s0[4];
   {
@@ -385,16 +416,20 @@ __device__ __forceinline__ void ss_quad(const float* ct, const Row& lm, const Ro
   for (int x = 0; x < 4; ++x) ss[x] = fmul(fsub(fmul(s0[x], el(a3, x)), el(m0.v, x)), el(bn, x));
 }
 
-__global__ void __launch_bounds__(kThreads2, 1)
+template <int LW, int NW1_, int SC_>
+__global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
               int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
               int g_lo, int g_hi, float omega, GosaSink g, int reset) {
+  using T = Tb2<LW, NW1_, SC_>;
+  constexpr int RPW = T::RPW, NW1 = T::NW1, NW2 = T::NW2, R1 = T::R1, TJ2 = T::TJ2,
+                QK = T::QK, TK2 = T::TK2, SC = T::SC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   unsigned char* p0ring = smem;
-  unsigned char* cring = p0ring + SP * kP0Slot;
-  float* p1ring = reinterpret_cast<float*>(cring + SC * kCSlot);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTb2Smem);
+  unsigned char* cring = p0ring + SP * T::kP0Slot;
+  float* p1ring = reinterpret_cast<float*>(cring + SC * T::kCSlot);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kSmem);
   uint64_t* pfull = bars;
   uint64_t* pempty = pfull + SP;
   uint64_t* cfull = pempty + SP;
@@ -403,22 +438,23 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   uint64_t* qempty = qfull + SQ;
   UnitRing* ring = reinterpret_cast<UnitRing*>(qempty + SQ);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
   Units units{ni, ktiles, ktiles * jtiles, chunk,
               (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], R1); }
-    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], R1 + TJ2); }
+    for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
+    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], NW1 + NW2); }
     // p1 ring: every thread arrives (no reliance on __syncwarp ordering for the
     // shared-memory rows written / read by other warps)
-    for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], R1 * 32); mbar_init(&qempty[s], TJ2 * 32); }
-    unit_ring_init(ring, R1 + TJ2);
+    for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], NW1 * 32); mbar_init(&qempty[s], NW2 * 32); }
+    unit_ring_init(ring, NW1 + NW2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   double acc = 0.0;
-  if (warp == R1 + TJ2) {
+  if (warp == NW1 + NW2) {
     // ------------------------------------------------------------- producer
     if (lane == 0) {
       uint32_t sp = 0, sc = 0;
@@ -432,8 +468,8 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         auto load_p0 = [&](int plane) {
           const int slot = sp % SP;
           if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
-          mbar_expect_tx(&pfull[slot], kP0Bytes);
-          tma_load_3d(p0ring + slot * kP0Slot, &maps.pin, &pfull[slot], k0 - 8, j0 - 2, plane);
+          mbar_expect_tx(&pfull[slot], T::kP0Bytes);
+          tma_load_3d(p0ring + slot * T::kP0Slot, &maps.pin, &pfull[slot], k0 - 8, j0 - 2, plane);
           ++sp;
         };
         load_p0(ia - 2);
@@ -442,16 +478,17 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
           load_p0(m + 1);
           const int slot = sc % SC;
           if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
-          mbar_expect_tx(&cfull[slot], NCOEF * kCExtBytes);
+          mbar_expect_tx(&cfull[slot], NCOEF * T::kCExtBytes);
           for (int c = 0; c < NCOEF; ++c)
-            tma_load_3d(cring + slot * kCSlot + c * kCExtBytes, &maps.coef[c], &cfull[slot],
+            tma_load_3d(cring + slot * T::kCSlot + c * T::kCExtBytes, &maps.coef[c], &cfull[slot],
                         k0 - 4, j0 - 1, m);
           ++sc;
         }
       }
     }
-  } else if (warp < R1) {
-    // ------------------------------------------------ step-1 warps (row j0-1+w)
+  } else if (warp < NW1) {
+    // ------------------------------------- step-1 warps (tile row r = j0-1+r)
+    const int r = warp * RPW + half;
     uint32_t sp = 0, sc = 0, sq = 0;
     Unit s;
     for (uint32_t n = 0;; ++n) {
@@ -460,8 +497,8 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
-      const int j1 = j0 - 1 + warp;
-      const int kq = k0 - 4 + lane * 4;
+      const int j1 = j0 - 1 + r;
+      const int kq = k0 - 4 + hl * 4;
       const bool row_in = j1 >= j_lo && j1 < j_hi;
       bool in1[4];
 #pragma unroll
@@ -470,9 +507,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       for (int w = 0; w < 2; ++w) {
         const int slot = sp % SP;
         mbar_wait(&pfull[slot], (sp / SP) & 1);
-        const float* pt = reinterpret_cast<const float*>(p0ring + slot * kP0Slot);
-        const Row x0 = load_row0(pt, warp, lane), x1 = load_row0(pt, warp + 1, lane),
-                  x2 = load_row0(pt, warp + 2, lane);
+        const float* pt = reinterpret_cast<const float*>(p0ring + slot * T::kP0Slot);
+        const Row x0 = load_row0<LW>(pt, r, hl), x1 = load_row0<LW>(pt, r + 1, hl),
+                  x2 = load_row0<LW>(pt, r + 2, hl);
         __syncwarp();
         if (lane == 0) mbar_arrive(&pempty[slot]);
         if (w == 0) { am = x0; a0 = x1; ap = x2; } else { bm = x0; b0 = x1; bp = x2; }
@@ -482,27 +519,27 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       for (int m = ia - 1; m <= ib; ++m) {
         const int pslot = sp % SP;
         mbar_wait(&pfull[pslot], (sp / SP) & 1);
-        const float* pt = reinterpret_cast<const float*>(p0ring + pslot * kP0Slot);
-        const Row cm = load_row0(pt, warp, lane), c0 = load_row0(pt, warp + 1, lane),
-                  cp = load_row0(pt, warp + 2, lane);
+        const float* pt = reinterpret_cast<const float*>(p0ring + pslot * T::kP0Slot);
+        const Row cm = load_row0<LW>(pt, r, hl), c0 = load_row0<LW>(pt, r + 1, hl),
+                  cp = load_row0<LW>(pt, r + 2, hl);
         __syncwarp();
         if (lane == 0) mbar_arrive(&pempty[pslot]);
         ++sp;
         const int cslot = sc % SC;
         mbar_wait(&cfull[cslot], (sc / SC) & 1);
-        const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot) + warp * QK + lane * 4;
+        const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + r * QK + hl * 4;
         // planes of the global interior (local indices): in a slab, step 1 also
         // recomputes the neighbours' adjacent planes (two-plane halos)
         const bool plane_in = m >= g_lo && m < g_hi;
-        float r[4];
+        float v[4];
         if (plane_in && row_in) {
           float ss[4];
-          ss_quad(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
+          ss_quad<QK * R1>(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
 #pragma unroll
-          for (int x = 0; x < 4; ++x) r[x] = in1[x] ? fadd(el(b0.v, x), fmul(omega, ss[x])) : el(b0.v, x);
+          for (int x = 0; x < 4; ++x) v[x] = in1[x] ? fadd(el(b0.v, x), fmul(omega, ss[x])) : el(b0.v, x);
         } else {
 #pragma unroll
-          for (int x = 0; x < 4; ++x) r[x] = el(b0.v, x);
+          for (int x = 0; x < 4; ++x) v[x] = el(b0.v, x);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty[cslot]);
@@ -511,7 +548,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         const int qslot = sq % SQ;
         if (sq >= (uint32_t)SQ) mbar_wait(&qempty[qslot], ((sq / SQ) - 1) & 1);
         float* q1 = p1ring + qslot * (QK * R1);
-        *reinterpret_cast<float4*>(q1 + warp * QK + lane * 4) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(q1 + r * QK + hl * 4) = make_float4(v[0], v[1], v[2], v[3]);
         mbar_arrive(&qfull[qslot]);   // release: publishes this thread's quad
         ++sq;
         am = bm; a0 = b0; ap = bp;
@@ -519,8 +556,8 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       }
     }
   } else {
-    // ------------------------------------------ step-2 warps (output row j0+w2)
-    const int w2 = warp - R1;
+    // -------------------------------------- step-2 warps (output row j0+r2)
+    const int r2 = (warp - NW1) * RPW + half;
     uint32_t sc = 0, sq = 0;
     Unit s;
     for (uint32_t n = 0;; ++n) {
@@ -529,21 +566,21 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
-      const int j = j0 + w2;
-      const int kq = k0 - 4 + lane * 4;
+      const int j = j0 + r2;
+      const int kq = k0 - 4 + hl * 4;
       const bool row_in = j < j_hi;
       bool in2[4];
 #pragma unroll
       for (int x = 0; x < 4; ++x) in2[x] = row_in && kq + x >= k_lo && kq + x < k_hi;
-      const bool writer = row_in && lane >= 1 && lane <= 30;
+      const bool writer = row_in && hl >= 1 && hl <= LW - 2;
       Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
 #pragma unroll 1
       for (int m = ia - 1; m <= ib; ++m) {
         const int qslot = sq % SQ;
         mbar_wait(&qfull[qslot], (sq / SQ) & 1);
         const float* q1 = p1ring + qslot * (QK * R1);
-        const Row nm = load_row1(q1, w2, lane), n0 = load_row1(q1, w2 + 1, lane),
-                  np = load_row1(q1, w2 + 2, lane);
+        const Row nm = load_row1<LW>(q1, r2, hl), n0 = load_row1<LW>(q1, r2 + 1, hl),
+                  np = load_row1<LW>(q1, r2 + 2, hl);
         mbar_arrive(&qempty[qslot]);  // this thread's reads of the slot are done
         ++sq;
         // coefficient stage of plane m (sequence sc): used at iteration m+1 for
@@ -551,9 +588,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         if (m >= ia + 1) {
           const int cslot = (sc - 1) % SC;          // stage of plane m-1
           mbar_wait(&cfull[cslot], ((sc - 1) / SC) & 1);
-          const float* ct = reinterpret_cast<const float*>(cring + cslot * kCSlot) + (w2 + 1) * QK + lane * 4;
+          const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + (r2 + 1) * QK + hl * 4;
           float ss[4];
-          ss_quad(ct, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
+          ss_quad<QK * R1>(ct, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
           float w[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
@@ -591,8 +628,8 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
 struct TmaState {
   StencilMaps base;          // coefficient maps + p map
   CUtensorMap scratch_map;   // p map of the rotation buffer
-  Tb2Maps tb2;               // two-step kernel: extended coefficient boxes + p map
-  CUtensorMap tb2_scratch;
+  Tb2Maps tb2[kTb2Shapes];   // two-step kernel shapes: coefficient boxes + p map
+  CUtensorMap tb2_scratch[kTb2Shapes];
   const float* p;
   const float* scratch;
 };
@@ -621,13 +658,17 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   }
   ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1]);
   ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1]);
-  for (int m = 0; m < NCOEF; ++m) {
+  auto encode_tb2 = [&](Tb2Maps& maps, CUtensorMap& scr, int qk, int r1) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    ok = ok && encode(&t->tb2.coef[m], F, F.f[fields[m]], QK, R1, pc[2]);
-  }
-  ok = ok && encode(&t->tb2.pin, F, F.f[HP_F_P], PW0, R1 + 2, pc[3]);
-  ok = ok && encode(&t->tb2_scratch, F, scratch, PW0, R1 + 2, pc[3]);
+    for (int m = 0; m < NCOEF; ++m) ok = ok && encode(&maps.coef[m], F, F.f[fields[m]], qk, r1, pc[2]);
+    ok = ok && encode(&maps.pin, F, F.f[HP_F_P], qk + 8, r1 + 2, pc[3]);
+    ok = ok && encode(&scr, F, scratch, qk + 8, r1 + 2, pc[3]);
+  };
+  encode_tb2(t->tb2[0], t->tb2_scratch[0], Tb2<32, 8, 4>::QK, Tb2<32, 8, 4>::R1);
+  encode_tb2(t->tb2[1], t->tb2_scratch[1], Tb2<16, 8, 4>::QK, Tb2<16, 8, 4>::R1);
+  encode_tb2(t->tb2[2], t->tb2_scratch[2], Tb2<16, 6, 5>::QK, Tb2<16, 6, 5>::R1);
+  encode_tb2(t->tb2[3], t->tb2_scratch[3], Tb2<16, 5, 6>::QK, Tb2<16, 5, 6>::R1);
   t->p = F.f[HP_F_P];
   t->scratch = scratch;
   if (!ok) {
@@ -681,6 +722,113 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// Two-step tile shapes (lanes per row, step-1 warps, coefficient slots):
+//   0 = (32, 8, 4): 128 x 8 step-1 tile, 120 x 6 outputs, 48 KB stages
+//   1 = (16, 8, 4):  64 x 16 step-1 tile, 56 x 14 outputs, 48 KB stages
+//   2 = (16, 6, 5):  64 x 12 step-1 tile, 56 x 10 outputs, 36 KB stages
+//   3 = (16, 5, 6):  64 x 10 step-1 tile, 56 x 8 outputs, 30 KB stages
+// The shape and the planes per work unit are chosen per pass geometry by a
+// scheduling model (tb2_choose below).
+static int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : -1;
+}
+
+template <int LW, int NW1, int SC>
+static long long tb2_tiles(int nj, int k_hi) {
+  using T = Tb2<LW, NW1, SC>;
+  return (long long)((k_hi + T::TK2 - 1) / T::TK2) * ((nj + T::TJ2 - 1) / T::TJ2);
+}
+
+// Makespan of one pass: the device-wide queue hands the chunk-major units to
+// the first free CTA (list scheduling); a unit of n planes takes n + 2 plane
+// steps (two warm-up planes) at the shape's per-step cost (microseconds per
+// plane step of one CTA, measured on the L grid: profiles/r01_tb2_shapes.txt).
+static double tb2_makespan(long long tiles, int ni, int chunk, int sms, double cost) {
+  std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+  const long long total = tiles * ((ni + chunk - 1) / chunk);
+  for (long long c = 0; c < std::min<long long>(sms, total); ++c) q.push(0.0);
+  double end = 0.0;
+  for (int c0 = 0; c0 < ni; c0 += chunk) {
+    const double d = (double)(std::min(chunk, ni - c0) + 2) * cost;
+    for (long long t = 0; t < tiles; ++t) {
+      const double f = q.top() + d;
+      q.pop();
+      q.push(f);
+      end = std::max(end, f);
+    }
+  }
+  return end;
+}
+
+// (shape, planes per unit) with the least predicted makespan, cached per pass
+// geometry; HIMENO_TB2_SHAPE / HIMENO_CHUNK pin either for sweeps.
+struct Tb2Choice {
+  int shape, chunk;
+};
+static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
+  static const double cost[kTb2Shapes] = {1.03, 1.04, 0.91, 0.885};
+  const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_CHUNK");
+  const bool pinned = pin_shape >= 0 || pin_chunk > 0;
+  static std::mutex mu;
+  static std::map<std::array<int, 4>, Tb2Choice> cache;
+  const std::array<int, 4> key{ni, nj, k_hi, sms};
+  if (!pinned) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  Tb2Choice best{1, 64};
+  double best_t = 1e300;
+  for (int v = 0; v < kTb2Shapes; ++v) {
+    if (pin_shape >= 0 && pin_shape < kTb2Shapes && v != pin_shape) continue;
+    long long tiles = 0;
+    switch (v) {
+      case 0: tiles = tb2_tiles<32, 8, 4>(nj, k_hi); break;
+      case 1: tiles = tb2_tiles<16, 8, 4>(nj, k_hi); break;
+      case 2: tiles = tb2_tiles<16, 6, 5>(nj, k_hi); break;
+      default: tiles = tb2_tiles<16, 5, 6>(nj, k_hi); break;
+    }
+    for (int chunk = 16; chunk <= 128; chunk += 8) {
+      const int ch = pin_chunk > 0 ? pin_chunk : chunk;
+      const double t = tb2_makespan(tiles, ni, ch, sms, cost[v]);
+      if (t < best_t) { best_t = t; best = {v, ch}; }
+      if (pin_chunk > 0) break;
+    }
+  }
+  if (!pinned) {
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = best;
+  }
+  return best;
+}
+
+template <int LW, int NW1, int SC>
+static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int i_lo, int i_hi,
+                      int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
+                      const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+  using T = Tb2<LW, NW1, SC>;
+  const int ktiles = (k_hi + T::TK2 - 1) / T::TK2;
+  const int jtiles = (j_hi - j_lo + T::TJ2 - 1) / T::TJ2;
+  const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
+  long long grid = sms;
+  if (grid > units) grid = units;
+  if (grid > g.capacity) return -1;
+  const size_t smem = T::smem_bytes();
+  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_stencil_tb2<LW, NW1, SC>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  k_stencil_tb2<LW, NW1, SC><<<(int)grid, T::kThreads, smem, s>>>(
+      maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, g_lo, g_hi, a.omega, g,
+      a.gosa_reset);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not
 // applicable: caller runs two single steps), or -1 on launch error.
 int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
@@ -695,29 +843,20 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (!full && (i_lo < 2 || i_hi > F.I - 2)) return 0;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   const int g_lo = 1 - a.i_off, g_hi = a.imax - 1 - a.i_off;
-  Tb2Maps maps = t->tb2;
-  if (p_in == t->scratch) maps.pin = t->tb2_scratch;
-  const int ktiles = (k_hi + TK2 - 1) / TK2;
-  const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const int chunk = chunk_planes(64);
-  const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
-  long long grid = sms;
-  if (grid > units) grid = units;
-  if (grid > g.capacity) return -1;
-  const size_t smem = 128 + (size_t)kTb2Smem + 2 * (SP + SC + SQ) * sizeof(uint64_t) +
-                      sizeof(UnitRing);
-  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_stencil_tb2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return -1;
-    attr = true;
+  const Tb2Choice c = tb2_choose(i_hi - i_lo, j_hi - j_lo, k_hi, sms);
+  const int v = c.shape;
+  Tb2Maps maps = t->tb2[v];
+  if (p_in == t->scratch) maps.pin = t->tb2_scratch[v];
+#define HP_TB2(LW, NW1, SC) \
+  launch_tb2<LW, NW1, SC>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, c.chunk, \
+                          a, g, s, sms)
+  switch (v) {
+    case 1: return HP_TB2(16, 8, 4);
+    case 2: return HP_TB2(16, 6, 5);
+    case 3: return HP_TB2(16, 5, 6);
+    default: return HP_TB2(32, 8, 4);
   }
-  k_stencil_tb2<<<(int)grid, kThreads2, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo,
-                                                   k_hi, ktiles, chunk, g_lo, g_hi, a.omega, g,
-                                                   a.gosa_reset);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+#undef HP_TB2
 }
 
 }  // namespace hp

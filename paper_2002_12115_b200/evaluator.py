@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import queue
 import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Optional
 
@@ -164,6 +165,15 @@ class B200Evaluator:
                 ctx.set_samples(sz.sample_points())
                 self._contexts[slot] = ctx
             return ctx
+
+    def prepare(self) -> None:
+        """Create every worker slot's device context now (concurrently), instead of
+        lazily at the slot's first evaluation."""
+        missing = [s for s in range(len(self.devices)) if s not in self._contexts]
+        if not missing:
+            return
+        with ThreadPoolExecutor(max_workers=len(missing)) as pool:
+            list(pool.map(self._context, missing))
 
     def _execute(self, genome):
         low = self.lowered(genome)

@@ -415,9 +415,9 @@ def main(argv=None) -> int:
     ap.add_argument("--ga-pop", type=int, default=20)
     ap.add_argument("--ga-gens", type=int, default=10)
     ap.add_argument("--ga-seed", type=int, default=0)
-    ap.add_argument("--ga-workers", type=int, default=0,
-                    help="concurrent evaluations per GPU (own context each); 0 = host cores "
-                         "(the reference GA uses max_concurrency = os.cpu_count())")
+    ap.add_argument("--ga-workers", type=int, default=4,
+                    help="concurrent evaluations per GPU (own context each); 4, 8 and 16 give "
+                         "the same evals/s (profiles/r01_ga_workers.jsonl); 0 = host cores")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

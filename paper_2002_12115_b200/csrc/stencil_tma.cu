@@ -53,9 +53,9 @@ constexpr uint32_t kPBytes = PW * PH * 4;                    // 5440
 constexpr uint32_t kPSlot = (kPBytes + 127) / 128 * 128;     // 5504
 constexpr uint32_t kCoefBytes = TK * TJ * 4;                 // 4096
 constexpr uint32_t kStageBytes = kPSlot + NCOEF * kCoefBytes;
-// planes per work unit: 32 for the single-step kernel, 64 for the two-step one
-// (measured, profiles/r01_chunk_sweep.txt, r01_tb2_chunk_sweep.txt);
-// HIMENO_CHUNK overrides both for sweeps
+// planes per work unit of the single-step kernel: 32 (measured,
+// profiles/r01_chunk_sweep.txt); HIMENO_CHUNK overrides it for sweeps.  The
+// two-step kernel chooses its own (tb2_choose).
 static int chunk_planes(int dflt) {
   static int env = -1;
   if (env < 0) {
@@ -762,13 +762,13 @@ static double tb2_makespan(long long tiles, int ni, int chunk, int sms, double c
 }
 
 // (shape, planes per unit) with the least predicted makespan, cached per pass
-// geometry; HIMENO_TB2_SHAPE / HIMENO_CHUNK pin either for sweeps.
+// geometry; HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK pin either for sweeps.
 struct Tb2Choice {
   int shape, chunk;
 };
 static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
   static const double cost[kTb2Shapes] = {1.03, 1.04, 0.91, 0.885};
-  const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_CHUNK");
+  const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_TB2_CHUNK");
   const bool pinned = pin_shape >= 0 || pin_chunk > 0;
   static std::mutex mu;
   static std::map<std::array<int, 4>, Tb2Choice> cache;

@@ -12,7 +12,7 @@ for sh in $SHAPES; do
   echo "shape=$sh pytest rc=$?" >> $OUT/pytest_s$sh.log
   tail -2 $OUT/pytest_s$sh.log
   for ch in 32 64; do
-  HIMENO_CHUNK=$ch HIMENO_TB2_SHAPE=$sh timeout 180 python -c "
+  HIMENO_TB2_CHUNK=$ch HIMENO_TB2_SHAPE=$sh timeout 180 python -c "
 import sys; sys.path.insert(0,'.')
 from paper_2002_12115_b200 import native as N
 from paper_2002_12115_b200.apps import himeno

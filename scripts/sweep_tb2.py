@@ -2,7 +2,7 @@
 
     python scripts/sweep_tb2.py > profiles/r01_tb2_shapes.txt
 
-HIMENO_TB2_SHAPE / HIMENO_CHUNK are read per launch (stencil_tma.cu tb2_choose), so
+HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK are read per launch (stencil_tma.cu tb2_choose), so
 they are set here between timings; the last line per grid is the automatic choice.
 """
 import os
@@ -32,11 +32,11 @@ def main():
             for shape in range(4):
                 for ch in CHUNKS:
                     os.environ["HIMENO_TB2_SHAPE"] = str(shape)
-                    os.environ["HIMENO_CHUNK"] = str(ch)
+                    os.environ["HIMENO_TB2_CHUNK"] = str(ch)
                     ms, gf = timed(c, sz)
                     print(f"{name} shape {shape} chunk {ch:3d} pass_ms {ms:.4f} GFLOPs {gf:.0f}", flush=True)
             os.environ.pop("HIMENO_TB2_SHAPE")
-            os.environ.pop("HIMENO_CHUNK")
+            os.environ.pop("HIMENO_TB2_CHUNK")
             ms, gf = timed(c, sz)
             print(f"{name} auto pass_ms {ms:.4f} GFLOPs {gf:.0f}", flush=True)
 

@@ -174,6 +174,33 @@ def test_every_stencil_config_bit_exact(gpu, name, nn):
         lib.hp_set_stencil_config(7)
 
 
+@pytest.mark.parametrize("shape", [0, 1, 2, 3])
+@pytest.mark.parametrize("chunk", [0, 16, 40])
+def test_two_step_shapes_bit_exact(gpu, monkeypatch, shape, chunk):
+    """Every compiled two-step tile shape, at the scheduler's unit length and at pinned
+    ones (HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK are read per launch), on a ragged grid whose
+    k and j extents are not multiples of any tile."""
+    sz = himeno.custom_size(75, 45, 141)
+    nn = 4
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    monkeypatch.setenv("HIMENO_TB2_SHAPE", str(shape))
+    if chunk:
+        monkeypatch.setenv("HIMENO_TB2_CHUNK", str(chunk))
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(1)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+            kt = ctx.time_jacobi(nn, 1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    assert kt.stencil_iters == 2.0
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+
+
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("name,nn", [("XS", 1), ("XS", 4), ("XS", 5), ("M", 2), ("M", 3),
                                       ("custom", 4), ("ragged", 3)])

@@ -187,6 +187,16 @@ int hp_read_gosa(hp_ctx* ctx, int side, double* out);
 int hp_jacobi_device(hp_ctx* ctx, int nn, int variant);
 int hp_jacobi_host(hp_ctx* ctx, const float* const* fields, int nn, int variant,
                    float* p_out, double* gosa_out);
+/* hp_jacobi_host_async: hp_jacobi_host without the final synchronisation: the
+ * copies and launches are enqueued on hp_stream(ctx) and the call returns;
+ * p_out and *gosa_out are valid after hp_sync(ctx).  With pinned host buffers
+ * the copies are asynchronous, so two contexts on one device pipeline
+ * consecutive jobs (one job's H2D overlaps the other's loop and D2H).  One
+ * outstanding call per context (HP_ERR_ARG otherwise).
+ * hp_sync: wait for everything enqueued on the context; deliver gosa. */
+int hp_jacobi_host_async(hp_ctx* ctx, const float* const* fields, int nn, int variant,
+                         float* p_out, double* gosa_out);
+int hp_sync(hp_ctx* ctx);
 /* Initialise the device mirrors to the program's post-initmt state on device. */
 int hp_init_device(hp_ctx* ctx);
 

@@ -37,6 +37,8 @@ struct hp_ctx {
   hp::Coherence coh[HP_NVARS];           // arrays: which side holds the latest data where
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;         // kernels launched by this context (all entry points)
+  double* pending_gosa = nullptr;  // hp_jacobi_host_async: where hp_sync delivers gosa
+  cudaEvent_t h2d_done = nullptr;  // end of this context's last host-input upload
   // slab decomposition (decomp.cpp): this context holds global planes
   // [i_off, i_off + I) of a gI-plane grid; stencil interior = local [li_lo, li_hi)
   int gI = 0, i_off = 0, li_lo = 1, li_hi = 0;

@@ -176,12 +176,16 @@ int hp::cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, what); \
   } while (0)
 
+static void forget_upload(hp_ctx* c);
+
 extern "C" void hp_destroy(hp_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  forget_upload(c);
+  if (c->h2d_done) cudaEventDestroy(c->h2d_done);
   if (c->dd) dd_destroy(c);
   if (c->dev.tma) destroy_stencil_tma(const_cast<void*>(c->dev.tma));
   if (c->slab) cudaFree(c->slab);
@@ -1180,28 +1184,99 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
   return rc;
 }
 
-extern "C" int hp_jacobi_host(hp_ctx* c, const float* const* fields, int nn, int variant,
-                              float* p_out, double* gosa_out) {
-  if (!c || !fields || !p_out || !gosa_out) {
-    set_error("hp_jacobi_host: null argument");
+// Host-input uploads of all contexts on one device are ordered through a
+// per-device token: each upload waits for the previous one (cudaStreamWaitEvent)
+// and publishes its own completion event.  PCIe is the shared resource, so
+// serialising uploads loses nothing, and it staggers concurrent jobs: the next
+// job's upload overlaps the current job's device loop instead of splitting the
+// link with it and then competing for the SMs at the same time.
+namespace {
+std::mutex g_upload_mu;
+cudaEvent_t g_last_upload[64] = {};
+}  // namespace
+
+static void forget_upload(hp_ctx* c) {
+  std::lock_guard<std::mutex> lock(g_upload_mu);
+  if (c->device >= 0 && c->device < 64 && g_last_upload[c->device] == c->h2d_done)
+    g_last_upload[c->device] = nullptr;
+}
+
+// Enqueue H2D of the inputs (through the staging buffer, repitched on device),
+// the device loop, D2H of p and of gosa into the pinned scalar slot; no host sync.
+static int jacobi_host_enqueue(hp_ctx* c, const float* const* fields, int nn, int variant,
+                               float* p_out, const char* who) {
+  if (!c || !fields || !p_out) {
+    set_error("%s: null argument", who);
     return HP_ERR_ARG;
   }
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   for (int f = 0; f < HP_NFIELDS; ++f) {
-    if (f == HP_F_WRK2) continue;
-    if (!fields[f]) {
-      set_error("hp_jacobi_host: field %d missing", f);
+    if (f != HP_F_WRK2 && !fields[f]) {
+      set_error("%s: field %d missing", who, f);
       return HP_ERR_ARG;
     }
-    CK(field_to_device(c, c->dev.f[f], fields[f]), "jacobi H2D");
+  }
+  if (!c->h2d_done)
+    CK(cudaEventCreateWithFlags(&c->h2d_done, cudaEventDisableTiming), "cudaEventCreate");
+  {
+    std::lock_guard<std::mutex> lock(g_upload_mu);
+    const bool tok = c->device >= 0 && c->device < 64;
+    if (tok && g_last_upload[c->device])
+      CK(cudaStreamWaitEvent(c->stream, g_last_upload[c->device], 0), "upload order");
+    for (int f = 0; f < HP_NFIELDS; ++f)
+      if (f != HP_F_WRK2) CK(field_to_device(c, c->dev.f[f], fields[f]), "jacobi H2D");
+    CK(cudaEventRecord(c->h2d_done, c->stream), "upload event");
+    if (tok) g_last_upload[c->device] = c->h2d_done;
   }
   int rc = hp_jacobi_device(c, nn, variant);
   if (rc != HP_OK) return rc;
   CK(field_to_host(c, p_out, c->dev.f[HP_F_P]), "jacobi D2H p");
-  CK(cudaMemcpyAsync(gosa_out, c->dscal + HP_V_GOSA * SLOT_BYTES, sizeof(double),
-                     cudaMemcpyDeviceToHost, c->stream),
+  CK(cudaMemcpyAsync(&c->hs<double>(HP_V_GOSA), c->dscal + HP_V_GOSA * SLOT_BYTES,
+                     sizeof(double), cudaMemcpyDeviceToHost, c->stream),
      "jacobi D2H gosa");
+  return HP_OK;
+}
+
+extern "C" int hp_jacobi_host(hp_ctx* c, const float* const* fields, int nn, int variant,
+                              float* p_out, double* gosa_out) {
+  if (!gosa_out) {
+    set_error("hp_jacobi_host: null argument");
+    return HP_ERR_ARG;
+  }
+  const int rc = jacobi_host_enqueue(c, fields, nn, variant, p_out, "hp_jacobi_host");
+  if (rc != HP_OK) return rc;
   CK(cudaStreamSynchronize(c->stream), "jacobi sync");
+  *gosa_out = c->hs<double>(HP_V_GOSA);
+  return HP_OK;
+}
+
+extern "C" int hp_jacobi_host_async(hp_ctx* c, const float* const* fields, int nn, int variant,
+                                    float* p_out, double* gosa_out) {
+  if (!gosa_out) {
+    set_error("hp_jacobi_host_async: null argument");
+    return HP_ERR_ARG;
+  }
+  if (c && c->pending_gosa) {
+    set_error("hp_jacobi_host_async: previous call not completed by hp_sync");
+    return HP_ERR_ARG;
+  }
+  const int rc = jacobi_host_enqueue(c, fields, nn, variant, p_out, "hp_jacobi_host_async");
+  if (rc != HP_OK) return rc;
+  c->pending_gosa = gosa_out;
+  return HP_OK;
+}
+
+extern "C" int hp_sync(hp_ctx* c) {
+  if (!c) {
+    set_error("hp_sync: null context");
+    return HP_ERR_ARG;
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(cudaStreamSynchronize(c->stream), "hp_sync");
+  if (c->pending_gosa) {
+    *c->pending_gosa = c->hs<double>(HP_V_GOSA);
+    c->pending_gosa = nullptr;
+  }
   return HP_OK;
 }
 

@@ -429,7 +429,10 @@ static int sm_count();
 int gosa_capacity_needed(const DevFields& F) {
   const int tiles = ((F.K + 127) / 128) * ((F.J + kTileWarps - 1) / kTileWarps);
   const int want = sm_count() * kTargetCtasPerSm * 2;
-  return kMaxCollapseBlocks + F.I + F.J + tiles + want + 1024;
+  // unit-queue kernels (stencil_tma.cu): one partial per work unit; the finest
+  // unit grid is 16 planes x 8 rows x 56 columns
+  const int units = ((F.I + 15) / 16) * ((F.J + 7) / 8) * ((F.K + 55) / 56);
+  return kMaxCollapseBlocks + F.I + F.J + tiles + want + units + 1024;
 }
 
 int launch_nest(Nest nest, Mapping map, const DevFields& F, const Box& box,

@@ -127,6 +127,7 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
   uint64_t* empty = full + S;
   UnitRing* ring = reinterpret_cast<UnitRing*>(empty + S);
+  __shared__ double unit_part[TJ];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
@@ -255,9 +256,11 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
         mm = nm; m0 = n0; mp = np;
       }
       (void)P;
+      unit_partial(g, u, acc, unit_part, warp, TJ, 1);
+      acc = 0.0;
     }
   }
-  gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
+  gosa_commit_units(g, units.count, reset);
 }
 
 // ================================================================ two-step kernel
@@ -437,6 +440,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   uint64_t* qfull = cempty + SC;
   uint64_t* qempty = qfull + SQ;
   UnitRing* ring = reinterpret_cast<UnitRing*>(qempty + SQ);
+  __shared__ double unit_part[NW2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
@@ -618,9 +622,11 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       }
       // stage of plane ib carries no output plane either
       if (lane == 0) mbar_arrive(&cempty[(sc - 1) % SC]);
+      unit_partial(g, u, acc, unit_part, warp - NW1, NW2, 1);
+      acc = 0.0;
     }
   }
-  gosa_commit(g, acc, gridDim.x, blockIdx.x, reset);
+  gosa_commit_units(g, units.count, reset);
 }
 
 // ------------------------------------------------------------------ host side
@@ -698,7 +704,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
-  if (grid > g.capacity) return -1;
+  if (units > g.capacity) return -1;   // one gosa partial per unit
   const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t) +
                       sizeof(UnitRing);
   if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
@@ -813,7 +819,7 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
-  if (grid > g.capacity) return -1;
+  if (units > g.capacity) return -1;   // one gosa partial per unit
   const size_t smem = T::smem_bytes();
   if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
   static bool attr = false;

@@ -98,6 +98,9 @@ SIGNATURES = {
     "hp_jacobi_device": (C.c_int, [_CtxP, C.c_int, C.c_int]),
     "hp_jacobi_host": (C.c_int, [_CtxP, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                  C.c_void_p, C.POINTER(C.c_double)]),
+    "hp_jacobi_host_async": (C.c_int, [_CtxP, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                 C.c_void_p, C.POINTER(C.c_double)]),
+    "hp_sync": (C.c_int, [_CtxP]),
     "hp_init_device": (C.c_int, [_CtxP]),
     "hp_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "hp_time_jacobi": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(KernelTimes)]),
@@ -315,3 +318,27 @@ class Context:
         check(self.lib.hp_jacobi_host(self.ptr, ptrs, nn, variant,
                                       C.c_void_p(p_out.ctypes.data), C.byref(g)), "hp_jacobi_host")
         return g.value
+
+    def jacobi_host_async(self, fields: dict, nn: int, variant: int, p_out) -> None:
+        """Enqueue jacobi_host without waiting; p_out (pinned for overlap) and gosa are
+        delivered by sync()."""
+        ptrs = (C.c_void_p * NFIELDS)()
+        for name, idx in FIELD_ID.items():
+            if name != "wrk2":
+                ptrs[idx] = fields[name].ctypes.data
+        g = C.c_double()
+        check(self.lib.hp_jacobi_host_async(self.ptr, ptrs, nn, variant,
+                                            C.c_void_p(p_out.ctypes.data), C.byref(g)),
+              "hp_jacobi_host_async")
+        # accepted: keep gosa's target and the host buffers alive until sync()
+        self._pending_gosa = g
+        self._pending_keep = (fields, p_out)
+
+    def sync(self):
+        """Wait for the context's queued work; returns the gosa of a pending
+        jacobi_host_async call (None if there was none)."""
+        check(self.lib.hp_sync(self.ptr), "hp_sync")
+        g = getattr(self, "_pending_gosa", None)
+        self._pending_gosa = None
+        self._pending_keep = None
+        return None if g is None else g.value

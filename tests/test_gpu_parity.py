@@ -12,6 +12,7 @@ from oracle import oracle
 from paper_2002_12115_b200 import native as N
 from paper_2002_12115_b200.apps import himeno
 from paper_2002_12115_b200.evaluator import B200Evaluator, MeasuredTime, valid_genomes
+from paper_2002_12115_b200.errors import TunerError
 from paper_2002_12115_b200.kinds import DirectiveKind
 
 pytestmark = pytest.mark.gpu
@@ -143,6 +144,65 @@ def test_jacobi_host_e2e(gpu):
         g = ctx.jacobi_host(inputs, nn, 1, p_out)
     assert np.array_equal(p_out, f["p"])
     assert abs(g - g64) <= GOSA_RTOL * g64
+
+
+def test_jacobi_host_async_pipeline(gpu):
+    """Two contexts alternating hp_jacobi_host_async jobs (the bench e2e pipeline) give
+    the serial call's results; a second async call before hp_sync is refused."""
+    name, nn = "S", 3
+    sz = himeno.size(name)
+    f = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(f)
+    inputs = {k: v.copy() for k, v in f.items()}
+    g64, _ = oracle.jacobi(f, nn)
+    outs = [np.empty_like(f["p"]), np.empty_like(f["p"])]
+    with N.Context(0, sz.I, sz.J, sz.K) as a, N.Context(0, sz.I, sz.J, sz.K) as b:
+        ctxs, got = (a, b), []
+        for step in range(5):
+            x = step % 2
+            if step >= 2:
+                got.append(ctxs[x].sync())
+            ctxs[x].jacobi_host_async(inputs, nn, 1, outs[x])
+        with pytest.raises(TunerError):
+            ctxs[0].jacobi_host_async(inputs, nn, 1, outs[0])
+        got += [a.sync(), b.sync()]
+        assert a.sync() is None
+    assert len(got) == 5
+    for g in got:
+        assert abs(g - g64) <= GOSA_RTOL * g64
+    for out in outs:
+        assert np.array_equal(out, f["p"])
+
+
+def test_gosa_bit_reproducible_under_concurrency(gpu):
+    """gosa of the unit-queue kernels is folded per work unit in unit order, so it is
+    bit-identical whichever CTA ran which unit: alone, and with a second context's
+    kernels competing for the SMs."""
+    sz = himeno.size("M")
+    with N.Context(0, sz.I, sz.J, sz.K) as a, N.Context(0, sz.I, sz.J, sz.K) as b:
+        ref = None
+        for tb in (1, 0):
+            lib = a.lib
+            old = lib.hp_set_temporal_blocking(tb)
+            try:
+                got = []
+                a.init_device()
+                a.jacobi_device(6, 1)
+                got.append(a.read_gosa(1))
+                for _ in range(3):
+                    a.init_device()
+                    b.init_device()
+                    b.jacobi_device(9, 1)      # enqueued on b's stream: runs concurrently
+                    a.jacobi_device(6, 1)
+                    got.append(a.read_gosa(1))
+                    b.sync()
+            finally:
+                lib.hp_set_temporal_blocking(old)
+            assert len(set(got)) == 1, got
+            if ref is None:
+                ref = got[0]
+            else:   # one- and two-step passes fold different units: equal to 1e-12
+                assert abs(got[0] - ref) <= GOSA_RTOL * ref
 
 
 def test_m_grid_selected_patterns(gpu):

@@ -4,7 +4,8 @@
 
 * kernels.cu   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
                --fmad=false (bit-exact with the host loops / oracle)
-* executor.cpp g++ -O3 -ffp-contract=off (no FMA contraction on the host loops)
+* executor.cpp g++ -O3 -march=x86-64-v3 -ffp-contract=off (AVX2 host loops, no FMA
+  contraction: every product and sum rounds separately, as on the device)
 * link         nvcc -shared -cudart static  ->  paper_2002_12115_b200/_native/
 
 The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
@@ -78,7 +79,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cpp")):
         obj = OUT_DIR / (src.stem + ".o")
-        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+        _run(["g++", "-O3", "-march=x86-64-v3", "-std=c++17", "-fPIC", "-ffp-contract=off",
+              "-fno-fast-math",
               "-Wall", "-Wno-unused-function", "-I", str(cuda / "include"), *inc,
               "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)

@@ -300,57 +300,89 @@ extern "C" int hp_set_samples(hp_ctx* c, int n, const int32_t* ijk) {
 // Same expression order as the C program; built with -ffp-contract=off so
 // every product and sum rounds separately, exactly like the kernels.
 
+// Row-wise: per (i, j) row each field is filled / computed over the k range with
+// restrict-qualified pointers, so the inner loops vectorise; values and their
+// order of rounding are those of the program's statements.
 static void host_init0(const HostFields& H, const Box& b) {
+  if (b.k1 <= b.k0) return;
+  const size_t n = (size_t)(b.k1 - b.k0) * sizeof(float);
   for (int i = b.i0; i < b.i1; ++i)
-    for (int j = b.j0; j < b.j1; ++j)
-      for (int k = b.k0; k < b.k1; ++k) {
-        const size_t c = H.at(i, j, k);
-        for (int f = 0; f < HP_NFIELDS; ++f)
-          if (f != HP_F_WRK2) H.f[f][c] = 0.0f;
-      }
+    for (int j = b.j0; j < b.j1; ++j) {
+      const size_t c = H.at(i, j, b.k0);
+      for (int f = 0; f < HP_NFIELDS; ++f)
+        if (f != HP_F_WRK2) memset(H.f[f] + c, 0, n);
+    }
+}
+
+static inline void fill_row(float* __restrict__ d, int n, float v) {
+  for (int k = 0; k < n; ++k) d[k] = v;
 }
 
 static void host_init1(const HostFields& H, const Box& b, int imax) {
   const float a3 = (float)(1.0 / 6.0);
+  const int n = b.k1 - b.k0;
+  if (n <= 0) return;
   for (int i = b.i0; i < b.i1; ++i) {
     const float pv = (float)(i * i) / (float)((imax - 1) * (imax - 1));
-    for (int j = b.j0; j < b.j1; ++j)
-      for (int k = b.k0; k < b.k1; ++k) {
-        const size_t c = H.at(i, j, k);
-        H.f[HP_F_A0][c] = 1.0f; H.f[HP_F_A1][c] = 1.0f; H.f[HP_F_A2][c] = 1.0f;
-        H.f[HP_F_A3][c] = a3;
-        H.f[HP_F_B0][c] = 0.0f; H.f[HP_F_B1][c] = 0.0f; H.f[HP_F_B2][c] = 0.0f;
-        H.f[HP_F_C0][c] = 1.0f; H.f[HP_F_C1][c] = 1.0f; H.f[HP_F_C2][c] = 1.0f;
-        H.f[HP_F_P][c] = pv;
-        H.f[HP_F_WRK1][c] = 0.0f;
-        H.f[HP_F_BND][c] = 1.0f;
-      }
+    for (int j = b.j0; j < b.j1; ++j) {
+      const size_t c = H.at(i, j, b.k0);
+      fill_row(H.f[HP_F_A0] + c, n, 1.0f);
+      fill_row(H.f[HP_F_A1] + c, n, 1.0f);
+      fill_row(H.f[HP_F_A2] + c, n, 1.0f);
+      fill_row(H.f[HP_F_A3] + c, n, a3);
+      fill_row(H.f[HP_F_B0] + c, n, 0.0f);
+      fill_row(H.f[HP_F_B1] + c, n, 0.0f);
+      fill_row(H.f[HP_F_B2] + c, n, 0.0f);
+      fill_row(H.f[HP_F_C0] + c, n, 1.0f);
+      fill_row(H.f[HP_F_C1] + c, n, 1.0f);
+      fill_row(H.f[HP_F_C2] + c, n, 1.0f);
+      fill_row(H.f[HP_F_P] + c, n, pv);
+      fill_row(H.f[HP_F_WRK1] + c, n, 0.0f);
+      fill_row(H.f[HP_F_BND] + c, n, 1.0f);
+    }
+  }
+}
+
+// One k row of the stencil: wrk2 and the ss*ss terms (vectorised: no
+// reduction in the loop); the caller sums the terms in k order.
+static void host_stencil_row(const float* __restrict__ p, const float* __restrict__ a0,
+                             const float* __restrict__ a1, const float* __restrict__ a2,
+                             const float* __restrict__ a3, const float* __restrict__ b0,
+                             const float* __restrict__ b1, const float* __restrict__ b2,
+                             const float* __restrict__ c0, const float* __restrict__ c1,
+                             const float* __restrict__ c2, const float* __restrict__ wrk1,
+                             const float* __restrict__ bnd, float* __restrict__ wrk2,
+                             float* __restrict__ t, int n, size_t R, size_t L, float omega) {
+  for (int k = 0; k < n; ++k) {
+    const float s0 = a0[k] * p[k + L] + a1[k] * p[k + R] + a2[k] * p[k + 1] +
+                     b0[k] * (p[k + L + R] - p[k + L - R] - p[k - L + R] + p[k - L - R]) +
+                     b1[k] * (p[k + R + 1] - p[k - R + 1] - p[k + R - 1] + p[k - R - 1]) +
+                     b2[k] * (p[k + L + 1] - p[k - L + 1] - p[k + L - 1] + p[k - L - 1]) +
+                     c0[k] * p[k - L] + c1[k] * p[k - R] + c2[k] * p[k - 1] + wrk1[k];
+    const float ss = (s0 * a3[k] - p[k]) * bnd[k];
+    t[k] = ss * ss;
+    wrk2[k] = p[k] + omega * ss;
   }
 }
 
 static double host_stencil(const HostFields& H, const Box& b, float omega) {
-  const float* p = H.f[HP_F_P];
-  const float *a0 = H.f[HP_F_A0], *a1 = H.f[HP_F_A1], *a2 = H.f[HP_F_A2], *a3 = H.f[HP_F_A3];
-  const float *b0 = H.f[HP_F_B0], *b1 = H.f[HP_F_B1], *b2 = H.f[HP_F_B2];
-  const float *c0 = H.f[HP_F_C0], *c1 = H.f[HP_F_C1], *c2 = H.f[HP_F_C2];
-  const float *wrk1 = H.f[HP_F_WRK1], *bnd = H.f[HP_F_BND];
-  float* wrk2 = H.f[HP_F_WRK2];
+  const int n = b.k1 - b.k0;
+  if (n <= 0) return 0.0;
   const size_t R = (size_t)H.K, L = (size_t)H.J * H.K;
+  std::vector<float> t((size_t)n);
   double acc = 0.0;
   for (int i = b.i0; i < b.i1; ++i)
-    for (int j = b.j0; j < b.j1; ++j)
-      for (int k = b.k0; k < b.k1; ++k) {
-        const size_t c = H.at(i, j, k);
-        const float s0 = a0[c] * p[c + L] + a1[c] * p[c + R] + a2[c] * p[c + 1] +
-                         b0[c] * (p[c + L + R] - p[c + L - R] - p[c - L + R] + p[c - L - R]) +
-                         b1[c] * (p[c + R + 1] - p[c - R + 1] - p[c + R - 1] + p[c - R - 1]) +
-                         b2[c] * (p[c + L + 1] - p[c - L + 1] - p[c + L - 1] + p[c - L - 1]) +
-                         c0[c] * p[c - L] + c1[c] * p[c - R] + c2[c] * p[c - 1] + wrk1[c];
-        const float ss = (s0 * a3[c] - p[c]) * bnd[c];
-        const float t = ss * ss;
-        acc += (double)t;
-        wrk2[c] = p[c] + omega * ss;
-      }
+    for (int j = b.j0; j < b.j1; ++j) {
+      const size_t c = H.at(i, j, b.k0);
+      // p is read through indices k - L .. k + L + R + 1 of the row base: pass the
+      // row base itself (negative offsets stay inside the array for interior rows)
+      host_stencil_row(H.f[HP_F_P] + c, H.f[HP_F_A0] + c, H.f[HP_F_A1] + c, H.f[HP_F_A2] + c,
+                       H.f[HP_F_A3] + c, H.f[HP_F_B0] + c, H.f[HP_F_B1] + c, H.f[HP_F_B2] + c,
+                       H.f[HP_F_C0] + c, H.f[HP_F_C1] + c, H.f[HP_F_C2] + c,
+                       H.f[HP_F_WRK1] + c, H.f[HP_F_BND] + c, H.f[HP_F_WRK2] + c, t.data(), n,
+                       R, L, omega);
+      for (int k = 0; k < n; ++k) acc += (double)t[k];   // k order, as the program
+    }
   return acc;
 }
 

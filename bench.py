@@ -139,6 +139,30 @@ def cpu_baseline(size, seconds: float, threads: int) -> dict:
                       f"{iters} iteration(s) after initmt, {threads} OpenMP threads, {el:.2f} s"}
 
 
+def reference_program(size):
+    """The program binary the reference's compile template produces (oracle/_ref, gcc -O2,
+    pragmas ignored, single-threaded), timed the way ExternalEvaluator times a run
+    (wall clock around the process, evaluators.py:207-214): nn=3 minus nn=1 = two Jacobi
+    iterations.  None when the binaries were not built (reference not mounted)."""
+    import subprocess
+    ref = ROOT / "oracle" / "_ref"
+    b1, b3 = ref / f"himeno_{size.name.lower()}_n1", ref / f"himeno_{size.name.lower()}_n3"
+    if not (b1.exists() and b3.exists()):
+        return None
+
+    def run(b):
+        t0 = time.perf_counter()
+        subprocess.run([str(b)], check=True, stdout=subprocess.DEVNULL)
+        return time.perf_counter() - t0
+
+    t1 = min(run(b1) for _ in range(2))
+    t3 = min(run(b3) for _ in range(2))
+    gf = FLOP_PER_POINT * size.interior_points * 2 / max(t3 - t1, 1e-9) / 1e9
+    return {"value": gf, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
+            "sample": f"oracle/_ref program ({size.name}, gcc -O2 -w, single-threaded): "
+                      f"wall(nn=3) {t3:.2f} s - wall(nn=1) {t1:.2f} s = 2 iterations"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
@@ -158,7 +182,7 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": "Himeno GFLOPS", "value": value, "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (Himeno initmt state)",
         "config": {"workload": f"himeno_{size.name}_jacobi", "grid": [size.I, size.J, size.K],
                    "nn_per_step": 1, "threads": threads},
@@ -169,6 +193,9 @@ def run_reference(args, world, rank):
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    prog = reference_program(size)
+    if prog is not None:
+        line["reference_program"] = prog
     if not args.no_ga:
         from oracle import ref_ga
         line["ga"] = ref_ga.ga_throughput(args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
@@ -177,11 +204,12 @@ def run_reference(args, world, rank):
     return 0
 
 
-def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, seed: int,
+def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: int,
                   workers: int = 1) -> dict:
     from paper_2002_12115_b200 import ga
     from paper_2002_12115_b200.evaluator import B200Evaluator
-    with B200Evaluator(size_name, nn=nn, devices=[device], workers_per_device=workers) as ev:
+    devices = [devices] if isinstance(devices, int) else list(devices)
+    with B200Evaluator(size_name, nn=nn, devices=devices, workers_per_device=workers) as ev:
         t_setup = time.perf_counter()
         ev.prepare()                                       # one device context per slot
         ev.measure((0,) * ev.gene_length)                  # first-touch warm-up
@@ -192,7 +220,7 @@ def ga_throughput(device: int, size_name: str, nn: int, pop: int, gens: int, see
         el = time.perf_counter() - t0
         ok = sum(1 for r in res.records for i in r.individuals if i.eval_source == "fresh")
     return {"size": size_name, "nn": nn, "population": pop, "generations": gens, "seed": seed,
-            "workers_per_gpu": workers, "setup_s": setup_s, "wall_s": el,
+            "gpus": len(devices), "workers_per_gpu": workers, "setup_s": setup_s, "wall_s": el,
             "fresh_evals": res.evaluations,
             "valid_fresh": ok,
             "evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
@@ -402,12 +430,17 @@ def run_ours(args, world, rank, local):
                 "iterations_per_launch": okt.stencil_iters,
                 "achieved_gbs": BYTES_STENCIL * osz.interior_points / (okt.stencil_ms / 1e3) / 1e9}
         extra["other_grids"] = others
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle
         extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
     if rank == 0 and not args.no_ga:
-        extra["ga"] = ga_throughput(local, args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
-                                    args.ga_seed, args.ga_workers or min(16, os.cpu_count() or 1))
+        # N > 1: the population is sharded over every GPU of the node (config 4), one
+        # worker slot per GPU, from rank 0's process
+        devices = [local] if world == 1 else list(range(world))
+        workers = (args.ga_workers or min(16, os.cpu_count() or 1)) if world == 1 else 1
+        extra["ga"] = ga_throughput(devices, args.ga_size, args.ga_nn, args.ga_pop,
+                                    args.ga_gens, args.ga_seed, workers)
+    barrier()   # the other ranks wait for rank 0's extras before tearing down NCCL
     if slab is not None:
         slab.close()
     else:
@@ -417,7 +450,7 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": "Himeno GFLOPS", "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Himeno initmt state, deterministic)",
             "config": {"workload": f"himeno_{size.name}_jacobi", "grid": [size.I, size.J, size.K],

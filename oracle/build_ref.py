@@ -8,7 +8,7 @@ all-CPU program; this script compiles the same C-subset text
 "gcc -O2 -w" (+ -mcmodel=medium for the >2 GiB static arrays of the large
 grids).  Outputs go to oracle/_ref/ only (git-ignored, travels with gpurun).
 
-    python oracle/build_ref.py [SIZE:NN ...]      default: XS:3 M:3 L:1
+    python oracle/build_ref.py [SIZE:NN ...]      default: XS:3 M:3 L:1 L:3
 """
 import subprocess
 import sys
@@ -21,7 +21,7 @@ from paper_2002_12115_b200.apps import himeno  # noqa: E402
 OUT = ROOT / "oracle" / "_ref"
 
 
-def build(cases=(("XS", 3), ("M", 3), ("L", 1))):
+def build(cases=(("XS", 3), ("M", 3), ("L", 1), ("L", 3))):
     OUT.mkdir(parents=True, exist_ok=True)
     built = []
     for name, nn in cases:

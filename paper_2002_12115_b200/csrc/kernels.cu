@@ -131,6 +131,13 @@ __device__ __forceinline__ void nest_point(const DevFields& F, int i, int j, int
 template <int NEST, int MAP>
 __global__ void __launch_bounds__(kNestThreads)
 k_nest(DevFields F, Box b, LaunchArgs a, GosaSink g) {
+  // launched with programmatic stream serialization: the next launch may be
+  // scheduled as soon as every block of this one started, and this one waits for
+  // its predecessor's completion (and memory) before touching any data -- the
+  // launches of an inner-loop gang (one per outer iteration) overlap their
+  // launch latency, never their data.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nk = (int)b.nk(), nj = (int)b.nj(), ni = (int)b.ni();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double acc = 0.0;
@@ -416,10 +423,21 @@ int launch_nest_t(Mapping map, const DevFields& F, const Box& b, const LaunchArg
     else blocks = (int)((b.nk() + kNestThreads - 1) / kNestThreads);
   }
   if (NEST == NEST_STENCIL && blocks > g.capacity) return -1;
-  if (map == MAP_COLLAPSE) k_nest<NEST, MAP_COLLAPSE><<<blocks, kNestThreads, 0, s>>>(F, b, a, g);
-  else if (map == MAP_GANG) k_nest<NEST, MAP_GANG><<<blocks, kNestThreads, 0, s>>>(F, b, a, g);
-  else k_nest<NEST, MAP_VECTOR><<<1, kNestThreads, 0, s>>>(F, b, a, g);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(map == MAP_VECTOR ? 1 : blocks);
+  cfg.blockDim = dim3(kNestThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (map == MAP_COLLAPSE) e = cudaLaunchKernelEx(&cfg, k_nest<NEST, MAP_COLLAPSE>, F, b, a, g);
+  else if (map == MAP_GANG) e = cudaLaunchKernelEx(&cfg, k_nest<NEST, MAP_GANG>, F, b, a, g);
+  else e = cudaLaunchKernelEx(&cfg, k_nest<NEST, MAP_VECTOR>, F, b, a, g);
+  return e == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace

@@ -79,6 +79,12 @@ __device__ void gosa_commit_units(const GosaSink& g, uint32_t nunits, int reset)
 __device__ void gosa_commit(const GosaSink& g, double v, int nblocks, int block_id, int reset) {
   __shared__ bool last;
   const double s = block_sum(v);
+  if (nblocks == 1) {
+    // single-block launch (a row of an inner-loop gang): no partials / ticket
+    // round trip; same sum as the last-block fold of one partial
+    if (threadIdx.x == 0) *g.slot = reset ? s : (*g.slot + s);
+    return;
+  }
   if (threadIdx.x == 0) {
     g.partials[block_id] = s;
     __threadfence();

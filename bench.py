@@ -17,8 +17,9 @@ GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
 * roofline   dominant kernel = the stencil launch; achieved = 56 B/pt * N_int /
              its CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline  the CPU oracle's jacobi on the same grid, all host threads.
-* ga         run_ga (pop 20 x gen 10, Himeno M, nn=3) with B200Evaluator on this
-             rank's GPU: fresh evaluations/s and generations/s.
+* ga         run_ga (config 4: pop 20 x gen 20, Himeno M, nn=3) with B200Evaluator on
+             this rank's GPU: fresh evaluations/s and generations/s; ga_config1 the
+             same for config 1 (Himeno XS, pop 4 x gen 4).
 
 N > 1 (torchrun): the grid is split into N slabs of i-planes (dd.SlabJacobi), one
 per GPU; halo planes and the gosa all-reduce go over NCCL; "scaling": "strong"
@@ -200,6 +201,7 @@ def run_reference(args, world, rank):
         from oracle import ref_ga
         line["ga"] = ref_ga.ga_throughput(args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
                                           args.ga_seed)
+        line["ga_config1"] = ref_ga.ga_throughput("XS", 3, 4, 4, args.ga_seed)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -440,6 +442,8 @@ def run_ours(args, world, rank, local):
         workers = (args.ga_workers or min(16, os.cpu_count() or 1)) if world == 1 else 1
         extra["ga"] = ga_throughput(devices, args.ga_size, args.ga_nn, args.ga_pop,
                                     args.ga_gens, args.ga_seed, workers)
+        # BASELINE config 1: Himeno XS, nn=3, pop 4 x gen 4
+        extra["ga_config1"] = ga_throughput(devices, "XS", 3, 4, 4, args.ga_seed, workers)
     barrier()   # the other ranks wait for rank 0's extras before tearing down NCCL
     if slab is not None:
         slab.close()
@@ -487,7 +491,7 @@ def main(argv=None) -> int:
     ap.add_argument("--ga-size", default="M")
     ap.add_argument("--ga-nn", type=int, default=3)
     ap.add_argument("--ga-pop", type=int, default=20)
-    ap.add_argument("--ga-gens", type=int, default=10)
+    ap.add_argument("--ga-gens", type=int, default=20)
     ap.add_argument("--ga-seed", type=int, default=0)
     ap.add_argument("--ga-workers", type=int, default=4,
                     help="concurrent evaluations per GPU (own context each); 4, 8 and 16 give "

@@ -35,6 +35,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "context.h"
@@ -977,12 +978,21 @@ extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
   }
   // fresh process: static arrays zero, device memory undefined (not timed)
   if (s->flags & HP_FLAG_FRESH_PROCESS) {
+    // zero the dirty host arrays, one thread per array (up to 8 at a time): the
+    // reset sits between two fitness runs of a GA worker slot, so it is kept short
     const size_t bytes = (size_t)c->I * c->J * c->K * sizeof(float);
+    std::vector<int> dirty;
     for (int f = 0; f < HP_NFIELDS; ++f)
-      if (c->host_dirty[f]) {
-        memset(c->host[f], 0, bytes);
-        c->host_dirty[f] = false;
-      }
+      if (c->host_dirty[f]) dirty.push_back(f);
+    const size_t nt = std::min<size_t>(8, dirty.size());
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (size_t x = t; x < dirty.size(); x += nt) memset(c->host[dirty[x]], 0, bytes);
+      });
+    for (size_t x = 0; nt && x < dirty.size(); x += nt) memset(c->host[dirty[x]], 0, bytes);
+    for (std::thread& th : pool) th.join();
+    for (int f : dirty) c->host_dirty[f] = false;
   }
   if (s->flags & HP_FLAG_POISON_DEVICE) {
     if (launch_fill(c->slab, c->field_stride * (HP_NFIELDS + 1), nanf(""), c->stream) < 0)

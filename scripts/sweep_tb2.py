@@ -14,6 +14,7 @@ from paper_2002_12115_b200 import native as N  # noqa: E402
 from paper_2002_12115_b200.apps import himeno  # noqa: E402
 
 CHUNKS = (24, 32, 40, 48, 64, 88, 96, 128)
+SHAPES = [int(x) for x in os.environ.get("SWEEP_SHAPES", "0,1,2,3,4").split(",")]
 
 
 def timed(ctx, sz):
@@ -29,7 +30,7 @@ def main():
         with N.Context(0, sz.I, sz.J, sz.K) as c:
             c.init_device()
             c.jacobi_device(4, 1)
-            for shape in range(4):
+            for shape in SHAPES:
                 for ch in CHUNKS:
                     os.environ["HIMENO_TB2_SHAPE"] = str(shape)
                     os.environ["HIMENO_TB2_CHUNK"] = str(ch)

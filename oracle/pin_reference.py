@@ -12,6 +12,11 @@ suite checks on any machine (the GPU box has no /root/reference):
   which must be identical (the pragmas are ignored by gcc).
 * plans_himeno.json.gz -- Planner.plan and Planner.plan_transfers
   (transfer.py:184-193, 413-418) for all 2^13 genomes.
+* ft_<class>.stdout -- the same for the NAS FT restatement (apps/ft.py) with the
+  template "gcc -O2 -w {src} -o {bin} -lm"; its checksums equal NPB's published
+  verification values (tests/test_ft.py).
+* plans_ft_s.json.gz -- Planner.plan / plan_transfers for FT class S on all 36
+  single-gene genomes, the all-ones genome and 400 seeded random genomes.
 * ga_streams.json -- run_ga (ga.py:183-211) GenerationRecord streams for
   several configs under a deterministic replay evaluator (fixed time table,
   including failures and timeouts).
@@ -38,7 +43,7 @@ from acctuner.evaluators import CommandConfig, ExternalEvaluator, MeasuredTime  
 from acctuner.ga import GAConfig, run_ga  # noqa: E402
 from acctuner.transfer import Planner  # noqa: E402
 
-from paper_2002_12115_b200.apps import himeno  # noqa: E402
+from paper_2002_12115_b200.apps import ft, himeno  # noqa: E402
 
 GOLDEN = ROOT / "tests" / "golden"
 CASES = [("XXS", 1), ("XXS", 3), ("XS", 3), ("XS", 1), ("S", 2), ("M", 2)]
@@ -137,11 +142,50 @@ def pin_ga():
     print(f"ga: {len(streams)} streams")
 
 
+FT_SAMPLES = 400
+
+
+def ft_genomes(n: int) -> list:
+    import random
+    rng = random.Random(2002_12115)
+    out = [tuple(int(i == j) for j in range(n)) for i in range(n)]
+    out.append((1,) * n)
+    out += [tuple(rng.randint(0, 1) for _ in range(n)) for _ in range(FT_SAMPLES)]
+    return out
+
+
+def pin_ft():
+    ev = ExternalEvaluator(CommandConfig("gcc -O2 -w {src} -o {bin} -lm", "{bin}", 600.0, 1),
+                           build_variant=None)
+    for name in ("S", "W"):
+        c = ft.ft_class(name)
+        fid, text = ft.source_file_id(c), ft.source_text(c)
+        out = ev.run_for_output({fid: text})
+        (GOLDEN / f"ft_{name.lower()}.stdout").write_text(out)
+        print(f"FT {name}: {out.split()[:2]} ...")
+    c = ft.ft_class("S")
+    proj = analyze_project([(ft.source_file_id(c), ft.source_text(c))])
+    elig = eligible_ids(classify_project(proj, StaticRuleProbe()))
+    planner = Planner(proj.loops, proj.refs, elig)
+    doc = {"file": ft.source_file_id(c), "eligible": elig, "plans": {}, "raw": {}}
+    for g in ft_genomes(len(elig)):
+        key = "".join(map(str, g))
+        doc["plans"][key] = [_sig(e) for e in planner.plan(g).entries]
+        doc["raw"][key] = [_sig(e) for e in planner.plan_transfers(g).entries]
+    with gzip.open(GOLDEN / "plans_ft_s.json.gz", "wt") as fh:
+        json.dump(doc, fh, separators=(",", ":"), sort_keys=True)
+    print(f"ft plans: {len(doc['plans'])} genomes")
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
+    if "--ft" in sys.argv:
+        pin_ft()
+        return
     pin_stdout()
     pin_plans()
     pin_ga()
+    pin_ft()
 
 
 if __name__ == "__main__":

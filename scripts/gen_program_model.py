@@ -20,7 +20,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from acctuner.classify import StaticRuleProbe, classify_project, eligible_ids  # noqa: E402
 from acctuner.code_model import analyze_project, dump_structural  # noqa: E402
 
-from paper_2002_12115_b200.apps import himeno  # noqa: E402
+from paper_2002_12115_b200.apps import ft, himeno  # noqa: E402
 
 
 def analyze(size_name, nn=3):
@@ -47,7 +47,30 @@ def shape_only(doc):
     return out
 
 
+def analyze_ft(cls_name):
+    c = ft.ft_class(cls_name)
+    proj = analyze_project([(ft.source_file_id(c), ft.source_text(c))])
+    verdicts = classify_project(proj, StaticRuleProbe())
+    doc = dump_structural(proj)
+    doc["index_var_keys"] = sorted(proj.refs.index_var_keys)
+    doc["verdicts"] = [v.to_json() for v in verdicts]
+    doc["eligible"] = eligible_ids(verdicts)
+    doc["generated_by"] = (f"scripts/gen_program_model.py: reference acctuner analyze_project + "
+                           f"StaticRuleProbe on ft.source_text('{c.name}')")
+    return doc
+
+
+def main_ft():
+    for name in ("S", "W"):
+        doc = analyze_ft(name)
+        out = ROOT / "paper_2002_12115_b200" / "apps" / "model" / f"ft_{name.lower()}.json"
+        out.write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")
+        print(f"wrote {out}: {sum(len(f['loops']) for f in doc['files'])} loops, "
+              f"gene length {len(doc['eligible'])}")
+
+
 def main():
+    main_ft()
     base = analyze("XS")
     for name in ("M", "L", "XL"):
         if shape_only(analyze(name)) != shape_only(base):

@@ -6,9 +6,11 @@ rejects pointers, structs and ``#define`` (code_model.py:286-366), so, as for Hi
 the program is restated in the accepted subset:
 
 * complex arrays are split into real / imaginary arrays (``u0r``/``u0i`` ...);
-* functions take no array or pointer arguments: the random-number state of NPB's
-  ``randlc(&x, a)`` lives in globals, and the FFT works in place on ``u1`` with
-  explicit copy loops where NPB's ``fft(dir, x1, x2)`` writes a second array;
+* one ``main``, every loop inline in execution order (the reference's planner is
+  lexical and does not follow calls): NPB's ``randlc`` / ``ipow46`` arithmetic is
+  written out, and each of the six ``cffts`` calls (3 forward, 3 inverse) is its
+  own loop block; the FFT works in place on ``u1`` with explicit copy loops where
+  NPB's ``fft(dir, x1, x2)`` writes a second array;
 * NPB's per-plane seed jump (``ipow46`` + ``randlc``) is a separate sequential loop
   that fills ``seeds[k]``, so the plane-fill loop carries no scalar across planes.
 
@@ -89,43 +91,103 @@ def source_file_id(c: FTClass) -> str:
     return f"ft_{c.name.lower()}.c"
 
 
-_CFFTS = """
-void cffts{d}(int is)
-{{
-  int a, b, c, m;
-  m = {logn};
-  for(a=0;a<{outer};a++){{
-    for(b=0;b<{n};b++)
-      for(c=0;c<{lines};c++){{
-        yr[b][c] = {xr};
-        yi[b][c] = {xi};
-      }}
-    cfftz(is, m, {n}, {lines});
-    for(b=0;b<{n};b++)
-      for(c=0;c<{lines};c++){{
-        {xr} = yr[b][c];
-        {xi} = yi[b][c];
-      }}
-  }}
-}}
-"""
+def _randlc(x: str, a: str, ind: str) -> str:
+    """Inline NPB randlc: x = a * x mod 2^46 (temporaries t1..t4, a1, a2, x1, x2, z)."""
+    return "\n".join(ind + l for l in [
+        f"t1 = r23 * {a};", "a1 = (int)(t1);", f"a2 = {a} - t23 * a1;",
+        f"t1 = r23 * {x};", "x1 = (int)(t1);", f"x2 = {x} - t23 * x1;",
+        "t1 = a1 * x2 + a2 * x1;", "t2 = (int)(r23 * t1);", "z = t1 - t23 * t2;",
+        "t3 = t23 * z + a2 * x2;", "t4 = (int)(r46 * t3);", f"{x} = t3 - t46 * t4;"])
+
+
+def _fft_block(n: int, outer: int, lines: int, xr: str, xi: str, sign: int, ind: str) -> str:
+    """One cffts: for every line batch a, copy lines into (yr, yi), Stockham radix-2 passes
+    (NPB fftz2) alternating y -> z -> y, copy back."""
+    m = log2i(n)
+    wi = "wi = ui[li + i];" if sign >= 1 else "wi = -ui[li + i];"
+
+    def butterfly(src, dst):
+        return f"""for(i=0;i<li;i++){{
+  i11 = i * lk;
+  i12 = i11 + {n // 2};
+  i21 = i * lj;
+  i22 = i21 + lk;
+  wr = ur[li + i];
+  {wi}
+  for(k=0;k<lk;k++)
+    for(j=0;j<{lines};j++){{
+      x11r = {src}r[i11 + k][j];
+      x11i = {src}i[i11 + k][j];
+      x21r = {src}r[i12 + k][j];
+      x21i = {src}i[i12 + k][j];
+      {dst}r[i21 + k][j] = x11r + x21r;
+      {dst}i[i21 + k][j] = x11i + x21i;
+      tr = x11r - x21r;
+      ti = x11i - x21i;
+      {dst}r[i22 + k][j] = wr * tr - wi * ti;
+      {dst}i[i22 + k][j] = wr * ti + wi * tr;
+    }}
+}}"""
+
+    def indent(t, n):
+        return "\n".join(" " * n + l for l in t.splitlines())
+
+    odd_copy = f"""
+  for(i=0;i<{n};i++)
+    for(j=0;j<{lines};j++){{
+      yr[i][j] = zr[i][j];
+      yi[i][j] = zi[i][j];
+    }}""" if m % 2 == 1 else ""
+    text = f"""for(a=0;a<{outer};a++){{
+  for(b=0;b<{n};b++)
+    for(c=0;c<{lines};c++){{
+      yr[b][c] = {xr};
+      yi[b][c] = {xi};
+    }}
+  for(l=1;l<={m};l++){{
+    lk = 1 << (l - 1);
+    li = 1 << ({m} - l);
+    lj = 2 * lk;
+    if(l % 2 == 1){{
+{indent(butterfly("y", "z"), 6)}
+    }} else {{
+{indent(butterfly("z", "y"), 6)}
+    }}
+  }}{odd_copy}
+  for(b=0;b<{n};b++)
+    for(c=0;c<{lines};c++){{
+      {xr} = yr[b][c];
+      {xi} = yi[b][c];
+    }}
+}}"""
+    return indent(text, len(ind))
 
 
 def source_text(c, niter: int | None = None) -> str:
-    """The FT program for class `c` (niter defaults to the class's)."""
+    """The FT program for class `c` (niter defaults to the class's).
+
+    One ``main`` with every loop inline, in execution order: the reference's planner
+    orders regions lexically and does not follow calls (code_model.py:847-887,
+    transfer.py:184-193), so a call inside a loop would hide the callee's writes from
+    its hoisting -- as in the Himeno text, statement order is execution order.
+    """
     c = ft_class(c)
     nx, ny, nz, nmax = c.nx, c.ny, c.nz, c.nmax
     niter = c.niter if niter is None else int(niter)
     decl = f"[{nz}][{ny}][{nx}]"
-    # line batches: x-lines of a z plane (c = j), y-lines of a z plane (c = i),
-    # z-lines of a y row (c = i); transform index b, line index c
-    cffts = (
-        _CFFTS.format(d=1, logn=log2i(nx), outer=nz, n=nx, lines=ny,
-                      xr="u1r[a][c][b]", xi="u1i[a][c][b]")
-        + _CFFTS.format(d=2, logn=log2i(ny), outer=nz, n=ny, lines=nx,
-                        xr="u1r[a][b][c]", xi="u1i[a][b][c]")
-        + _CFFTS.format(d=3, logn=log2i(nz), outer=ny, n=nz, lines=nx,
-                        xr="u1r[b][a][c]", xi="u1i[b][a][c]"))
+    pad = "  "
+
+    def ffts(sign):
+        # line batches: x-lines of a z plane (c = j), y-lines of a z plane (c = i),
+        # z-lines of a y row (c = i); transform index b, line index c
+        b1 = _fft_block(nx, nz, ny, "u1r[a][c][b]", "u1i[a][c][b]", sign, pad)
+        b2 = _fft_block(ny, nz, nx, "u1r[a][b][c]", "u1i[a][b][c]", sign, pad)
+        b3 = _fft_block(nz, ny, nx, "u1r[b][a][c]", "u1i[b][a][c]", sign, pad)
+        return [b1, b2, b3] if sign >= 1 else [b3, b2, b1]
+
+    fwd = "\n".join(ffts(1))
+    inv = "\n".join("\n".join("  " + l for l in blk.splitlines()) for blk in ffts(-1))
+    seed_step = _randlc("rx", "an", "    ")
     return f"""static double u0r{decl};
 static double u0i{decl};
 static double u1r{decl};
@@ -142,34 +204,17 @@ static double zi[{nmax}][{nmax}];
 static double seeds[{nz}];
 static double sumr[{niter + 1}];
 static double sumi[{niter + 1}];
-static double rx, ra;
 
-double randlc()
+int main()
 {{
+  int i, j, k, a, b, c, l, lk, li, lj, i11, i12, i21, i22, ii, jj, kk, n, n2, ln, it, q, r, s;
+  double ap, an, x, pq, pr, rx, t, ti, tr, wr, wi, x11r, x11i, x21r, x21i, cr, ci;
   double r23, r46, t23, t46, t1, t2, t3, t4, a1, a2, x1, x2, z;
+  double xa1, xa2, xx1, xx2, tt1, tt2, tt3, tt4, zz;
   r23 = 1.1920928955078125e-07;
   r46 = r23 * r23;
   t23 = 8388608.0;
   t46 = t23 * t23;
-  t1 = r23 * ra;
-  a1 = (int)(t1);
-  a2 = ra - t23 * a1;
-  t1 = r23 * rx;
-  x1 = (int)(t1);
-  x2 = rx - t23 * x1;
-  t1 = a1 * x2 + a2 * x1;
-  t2 = (int)(r23 * t1);
-  z = t1 - t23 * t2;
-  t3 = t23 * z + a2 * x2;
-  t4 = (int)(r46 * t3);
-  rx = t3 - t46 * t4;
-  return r46 * rx;
-}}
-
-void compute_indexmap()
-{{
-  int i, j, k, ii, jj, kk;
-  double ap;
   ap = -4.0 * 1.0e-6 * 3.141592653589793238 * 3.141592653589793238;
   for(k=0;k<{nz};k++)
     for(j=0;j<{ny};j++)
@@ -179,45 +224,25 @@ void compute_indexmap()
         ii = ((i + {nx // 2}) % {nx}) - {nx // 2};
         twid[k][j][i] = exp(ap * (double)(ii * ii + jj * jj + kk * kk));
       }}
-}}
-
-void compute_initial_conditions()
-{{
-  int i, j, k, n, n2;
-  double an, q, r, x, xa1, xa2, xx1, xx2, tt1, tt2, tt3, tt4, zz;
-  double r23, r46, t23, t46;
-  r23 = 1.1920928955078125e-07;
-  r46 = r23 * r23;
-  t23 = 8388608.0;
-  t46 = t23 * t23;
-  q = 1220703125.0;
-  r = 1.0;
+  pq = 1220703125.0;
+  pr = 1.0;
   n = {2 * nx * ny};
   while(n > 1){{
     n2 = n / 2;
     if(n2 * 2 == n){{
-      rx = q;
-      ra = q;
-      randlc();
-      q = rx;
+{_randlc("pq", "pq", "      ")}
       n = n2;
     }} else {{
-      rx = r;
-      ra = q;
-      randlc();
-      r = rx;
+{_randlc("pr", "pq", "      ")}
       n = n - 1;
     }}
   }}
-  rx = r;
-  ra = q;
-  randlc();
-  an = rx;
+{_randlc("pr", "pq", "  ")}
+  an = pr;
   rx = 314159265.0;
-  ra = an;
   for(k=0;k<{nz};k++){{
     seeds[k] = rx;
-    randlc();
+{seed_step}
   }}
   xa1 = (int)(r23 * 1220703125.0);
   xa2 = 1220703125.0 - t23 * xa1;
@@ -245,12 +270,6 @@ void compute_initial_conditions()
         u1i[k][j][i] = r46 * x;
       }}
   }}
-}}
-
-void fft_init()
-{{
-  int i, j, ln;
-  double t, ti;
   ur[0] = {log2i(nmax)};
   ui[0] = 0.0;
   ln = 1;
@@ -263,117 +282,7 @@ void fft_init()
     }}
     ln = 2 * ln;
   }}
-}}
-
-void cfftz(int is, int m, int n, int nl)
-{{
-  int l, i, k, j, lk, li, lj, i11, i12, i21, i22, n1;
-  double wr, wi, x11r, x11i, x21r, x21i, tr, ti;
-  n1 = n / 2;
-  for(l=1;l<=m;l++){{
-    lk = 1 << (l - 1);
-    li = 1 << (m - l);
-    lj = 2 * lk;
-    if(l % 2 == 1){{
-      for(i=0;i<li;i++){{
-        i11 = i * lk;
-        i12 = i11 + n1;
-        i21 = i * lj;
-        i22 = i21 + lk;
-        wr = ur[li + i];
-        wi = ui[li + i];
-        if(is < 1){{
-          wi = -wi;
-        }}
-        for(k=0;k<lk;k++)
-          for(j=0;j<nl;j++){{
-            x11r = yr[i11 + k][j];
-            x11i = yi[i11 + k][j];
-            x21r = yr[i12 + k][j];
-            x21i = yi[i12 + k][j];
-            zr[i21 + k][j] = x11r + x21r;
-            zi[i21 + k][j] = x11i + x21i;
-            tr = x11r - x21r;
-            ti = x11i - x21i;
-            zr[i22 + k][j] = wr * tr - wi * ti;
-            zi[i22 + k][j] = wr * ti + wi * tr;
-          }}
-      }}
-    }} else {{
-      for(i=0;i<li;i++){{
-        i11 = i * lk;
-        i12 = i11 + n1;
-        i21 = i * lj;
-        i22 = i21 + lk;
-        wr = ur[li + i];
-        wi = ui[li + i];
-        if(is < 1){{
-          wi = -wi;
-        }}
-        for(k=0;k<lk;k++)
-          for(j=0;j<nl;j++){{
-            x11r = zr[i11 + k][j];
-            x11i = zi[i11 + k][j];
-            x21r = zr[i12 + k][j];
-            x21i = zi[i12 + k][j];
-            yr[i21 + k][j] = x11r + x21r;
-            yi[i21 + k][j] = x11i + x21i;
-            tr = x11r - x21r;
-            ti = x11i - x21i;
-            yr[i22 + k][j] = wr * tr - wi * ti;
-            yi[i22 + k][j] = wr * ti + wi * tr;
-          }}
-      }}
-    }}
-  }}
-  if(m % 2 == 1){{
-    for(i=0;i<n;i++)
-      for(j=0;j<nl;j++){{
-        yr[i][j] = zr[i][j];
-        yi[i][j] = zi[i][j];
-      }}
-  }}
-}}
-{cffts}
-void evolve()
-{{
-  int i, j, k;
-  for(k=0;k<{nz};k++)
-    for(j=0;j<{ny};j++)
-      for(i=0;i<{nx};i++){{
-        u0r[k][j][i] = u0r[k][j][i] * twid[k][j][i];
-        u0i[k][j][i] = u0i[k][j][i] * twid[k][j][i];
-        u1r[k][j][i] = u0r[k][j][i];
-        u1i[k][j][i] = u0i[k][j][i];
-      }}
-}}
-
-void checksum(int it)
-{{
-  int j, q, r, s;
-  double cr, ci;
-  cr = 0.0;
-  ci = 0.0;
-  for(j=1;j<=1024;j++){{
-    q = j % {nx};
-    r = (3 * j) % {ny};
-    s = (5 * j) % {nz};
-    cr = cr + u2r[s][r][q];
-    ci = ci + u2i[s][r][q];
-  }}
-  sumr[it] = cr / {float(c.points)!r};
-  sumi[it] = ci / {float(c.points)!r};
-}}
-
-int main()
-{{
-  int i, j, k, it;
-  compute_indexmap();
-  compute_initial_conditions();
-  fft_init();
-  cffts1(1);
-  cffts2(1);
-  cffts3(1);
+{fwd}
   for(k=0;k<{nz};k++)
     for(j=0;j<{ny};j++)
       for(i=0;i<{nx};i++){{
@@ -381,17 +290,32 @@ int main()
         u0i[k][j][i] = u1i[k][j][i];
       }}
   for(it=1;it<={niter};it++){{
-    evolve();
-    cffts3(-1);
-    cffts2(-1);
-    cffts1(-1);
+    for(k=0;k<{nz};k++)
+      for(j=0;j<{ny};j++)
+        for(i=0;i<{nx};i++){{
+          u0r[k][j][i] = u0r[k][j][i] * twid[k][j][i];
+          u0i[k][j][i] = u0i[k][j][i] * twid[k][j][i];
+          u1r[k][j][i] = u0r[k][j][i];
+          u1i[k][j][i] = u0i[k][j][i];
+        }}
+{inv}
     for(k=0;k<{nz};k++)
       for(j=0;j<{ny};j++)
         for(i=0;i<{nx};i++){{
           u2r[k][j][i] = u1r[k][j][i];
           u2i[k][j][i] = u1i[k][j][i];
         }}
-    checksum(it);
+    cr = 0.0;
+    ci = 0.0;
+    for(j=1;j<=1024;j++){{
+      q = j % {nx};
+      r = (3 * j) % {ny};
+      s = (5 * j) % {nz};
+      cr = cr + u2r[s][r][q];
+      ci = ci + u2i[s][r][q];
+    }}
+    sumr[it] = cr / {float(c.points)!r};
+    sumi[it] = ci / {float(c.points)!r};
   }}
   for(it=1;it<={niter};it++){{
     printf("%.12e\\n", sumr[it]);

@@ -8,7 +8,11 @@
   contraction: every product and sum rounds separately, as on the device)
 * link         nvcc -shared -cudart static  ->  paper_2002_12115_b200/_native/
 
-The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
+Generated executors (codegen.py; generic.APPS): for every application text with a
+committed program model, ``gen/<app>.cu`` is generated and compiled the same way
+into ``_native/libapp_<app>.so``.
+
+The .so files are git-ignored but travel to the GPU box with the gpurun snapshot.
 Rebuilds only when a source or header is newer than the library.
 """
 
@@ -63,7 +67,46 @@ def _run(cmd: list, verbose: bool) -> None:
         print(proc.stdout + proc.stderr, flush=True)
 
 
+GEN_DIR = PKG / "gen"
+
+
+def _gen_inputs() -> list:
+    return [PKG / "codegen.py", CSRC / "gen_runtime.cuh", INCLUDE / "app_b200.h",
+            PKG / "apps" / "ft.py", PKG / "apps" / "himeno.py", Path(__file__)] + \
+        sorted((PKG / "apps" / "model").glob("*.json"))
+
+
+def build_apps(force: bool = False, verbose: bool = False) -> list:
+    """Generate and compile every generated executor (generic.APPS)."""
+    from . import codegen, generic
+    cuda = _cuda_home()
+    nvcc = str(cuda / "bin" / "nvcc")
+    OUT_DIR.mkdir(exist_ok=True)
+    GEN_DIR.mkdir(exist_ok=True)
+    newest = max(p.stat().st_mtime for p in _gen_inputs())
+    specs = generic.app_specs()
+    out = []
+    for name in generic.APPS:
+        lib = generic.lib_path(name)
+        out.append(lib)
+        if not force and lib.exists() and lib.stat().st_mtime >= newest:
+            continue
+        spec = specs[name]
+        prog = spec.program()
+        kinds = {lid: k.value for lid, k in prog.kinds.items()}
+        src = GEN_DIR / f"{name}.cu"
+        src.write_text(codegen.generate(name, spec.text(), prog.model, kinds))
+        tmp = lib.with_suffix(".so.tmp")
+        _run([nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-diag-suppress", "177,550,549",
+              "-I", str(INCLUDE), "-I", str(CSRC), "-shared", "-cudart", "static",
+              "-o", str(tmp), str(src)], verbose)
+        os.replace(tmp, lib)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_apps(force, verbose)
     if not force and not _stale():
         return LIB
     cuda = _cuda_home()

@@ -1,0 +1,706 @@
+"""Generic B200 executor generator: a C-subset program -> one CUDA translation unit.
+
+The hand-written Himeno library (csrc/) covers the headline application.  Any
+other program the reference can tune (its parser's C subset, acctuner/
+code_model.py:1-12) goes through this generator instead, which does at build
+time what an OpenACC compiler does for every directive the gene can select
+(emitter.py:132-228 inserts them, PGI compiles them):
+
+* the program becomes a C++ struct ``Prog``: globals are members (one instance
+  per device context, zeroed before each run like a fresh process's statics),
+  functions are member functions with their bodies unchanged -- except that
+  every ``for`` statement (loop id L, reference numbering) is wrapped as
+
+      { R.before(L); if (R.dev(L)) { <launch of k_L> } else for (...) ...; R.after(L); }
+
+  so one compiled program runs any gene pattern: gene = 0 loops execute the
+  original host code, gene = 1 loops launch their kernel, and the transfer
+  plan's events fire at the loop hooks (runtime: csrc/gen_runtime.cuh);
+* each eligible loop gets one sm_100a kernel ``k_L`` whose body is the loop's
+  own source text over device arrays of the same names.  Directive kinds map
+  to launches as OpenACC defines them: ``kernels`` collapses the tight
+  rectangular nest below L into one grid (a loop with a loop-carried scalar
+  runs as one sequential device thread, as an auto-parallelising compiler
+  leaves it), ``parallel loop`` spreads L's iterations over the grid,
+  ``parallel loop vector`` runs them in one thread block.  Scalars are
+  firstprivate kernel arguments; ``s = s + e`` / ``s += e`` accumulations are
+  reductions (fp64 block partials, folded in block order on the host).
+
+Parsing is limited to what the generator needs (declarations, function
+headers, ``for`` headers, identifier use); loop ids, spans, nesting and shapes
+come from the reference's own front-end (the committed program model).
+"""
+
+from __future__ import annotations
+
+import re
+from dataclasses import dataclass, field
+from typing import Optional
+
+TYPE_WORDS = ("void", "int", "long", "short", "char", "float", "double", "unsigned", "signed")
+KEYWORDS = set(TYPE_WORDS) | {"static", "const", "register", "for", "while", "if", "else",
+                              "return", "break", "continue", "sizeof"}
+MATH = {"sqrt", "fabs", "sin", "cos", "tan", "exp", "log", "pow", "floor", "ceil", "fmin",
+        "fmax", "abs", "printf"}
+
+_TOKEN = re.compile(r"""
+    (?P<ws>\s+|//[^\n]*|/\*.*?\*/)
+  | (?P<num>(?:\d+\.\d*|\.\d+|\d+)(?:[eE][+-]?\d+)?[uUlLfF]*)
+  | (?P<name>[A-Za-z_]\w*)
+  | (?P<str>"(?:\\.|[^"\\])*")
+  | (?P<chr>'(?:\\.|[^'\\])*')
+  | (?P<punct><<=|>>=|\+\+|--|\+=|-=|\*=|/=|%=|==|!=|<=|>=|&&|\|\||<<|>>|[-+*/%<>=!&|^~?:;,()\[\]{}.])
+""", re.S | re.X)
+
+
+@dataclass
+class Tok:
+    kind: str
+    text: str
+    pos: int
+
+
+def tokenize(text: str) -> list:
+    out, i = [], 0
+    while i < len(text):
+        m = _TOKEN.match(text, i)
+        if not m:
+            raise ValueError(f"codegen: cannot tokenize at {i}: {text[i:i + 20]!r}")
+        if m.lastgroup != "ws":
+            out.append(Tok(m.lastgroup, m.group(), i))
+        i = m.end()
+    return out
+
+
+@dataclass
+class Decl:
+    name: str
+    ctype: str
+    dims: list            # [] scalar
+
+    @property
+    def is_array(self) -> bool:
+        return bool(self.dims)
+
+    def elems(self) -> int:
+        n = 1
+        for d in self.dims:
+            n *= d
+        return n
+
+
+@dataclass
+class Func:
+    name: str
+    ret: str
+    params: list          # [Decl]
+    body: tuple           # (start, end) of "{ ... }"
+    locals: list = field(default_factory=list)
+
+    def scalar(self, name: str) -> Optional[Decl]:
+        for d in self.params + self.locals:
+            if d.name == name:
+                return d
+        return None
+
+
+def _match(toks, i, close):
+    opener = toks[i].text
+    depth = 0
+    for j in range(i, len(toks)):
+        if toks[j].text == opener:
+            depth += 1
+        elif toks[j].text == close:
+            depth -= 1
+            if depth == 0:
+                return j
+    raise ValueError(f"codegen: unbalanced {opener!r}")
+
+
+def _declarators(toks, i, ctype):
+    """Parse `a, b[3][4], c;` starting at i; returns ([Decl], index after ';')."""
+    out = []
+    while True:
+        name = toks[i].text
+        i += 1
+        dims = []
+        while toks[i].text == "[":
+            dims.append(int(toks[i + 1].text.rstrip("uUlL")))
+            i += 3
+        if toks[i].text == "=":
+            raise ValueError(f"codegen: initialised declaration of {name} is not supported")
+        out.append(Decl(name, ctype, dims))
+        if toks[i].text == ";":
+            return out, i + 1
+        if toks[i].text != ",":
+            raise ValueError(f"codegen: bad declaration near {name}")
+        i += 1
+
+
+class CProgram:
+    """Globals and functions of a C-subset program text."""
+
+    def __init__(self, text: str):
+        self.text = text
+        self.toks = tokenize(text)
+        self.globals: list = []
+        self.funcs: list = []
+        toks, i = self.toks, 0
+        while i < len(toks):
+            j = i
+            while toks[j].text in ("static", "const", "register"):
+                j += 1
+            tparts = []
+            while toks[j].kind == "name" and toks[j].text in TYPE_WORDS:
+                tparts.append(toks[j].text)
+                j += 1
+            if not tparts:
+                raise ValueError(f"codegen: expected a declaration at {toks[i].pos}")
+            ctype = " ".join(tparts)
+            if toks[j + 1].text == "(":
+                name = toks[j].text
+                close = _match(toks, j + 1, ")")
+                params = []
+                k = j + 2
+                while k < close:
+                    ptype = []
+                    while toks[k].text in TYPE_WORDS:
+                        ptype.append(toks[k].text)
+                        k += 1
+                    if ptype == ["void"] and k == close:
+                        break
+                    params.append(Decl(toks[k].text, " ".join(ptype), []))
+                    k += 1
+                    if toks[k].text == ",":
+                        k += 1
+                b0 = close + 1
+                b1 = _match(toks, b0, "}")
+                f = Func(name, ctype, params, (toks[b0].pos, toks[b1].pos + 1))
+                self._locals(f, b0, b1)
+                self.funcs.append(f)
+                i = b1 + 1
+            else:
+                decls, i = _declarators(toks, j, ctype)
+                self.globals.extend(decls)
+        self.gmap = {d.name: d for d in self.globals}
+
+    def _locals(self, f: Func, b0: int, b1: int):
+        toks, k, depth = self.toks, b0 + 1, 1
+        while k < b1:
+            t = toks[k].text
+            if t == "{":
+                depth += 1
+            elif t == "}":
+                depth -= 1
+            if depth == 1 and toks[k].kind == "name" and t in TYPE_WORDS and \
+                    (k == b0 + 1 or toks[k - 1].text in (";", "{", "}")):
+                tparts = []
+                while toks[k].text in TYPE_WORDS:
+                    tparts.append(toks[k].text)
+                    k += 1
+                decls, k = _declarators(toks, k, " ".join(tparts))
+                if any(d.is_array for d in decls):
+                    raise ValueError(f"codegen: local arrays in {f.name} are not supported")
+                f.locals.extend(decls)
+                continue
+            k += 1
+
+    def func_at(self, pos: int) -> Func:
+        for f in self.funcs:
+            if f.body[0] <= pos < f.body[1]:
+                return f
+        raise ValueError(f"codegen: position {pos} is outside every function")
+
+    def toks_in(self, a: int, b: int) -> list:
+        return [t for t in self.toks if a <= t.pos < b]
+
+
+# ---------------------------------------------------------------------------- loops
+
+@dataclass
+class Header:
+    var: str
+    lo: str               # C expression
+    hi: str               # exclusive upper bound expression
+    step: int
+    body: tuple           # (start, end) of the body statement
+
+
+def parse_header(prog: CProgram, span) -> Optional[Header]:
+    """`for(v = lo; v < hi | v <= hi; v++ | ++v | v += c | v = v + c) body`."""
+    a, b = span
+    toks = prog.toks_in(a, b)
+    if not toks or toks[0].text != "for" or toks[1].text != "(":
+        return None
+    close = _match(toks, 1, ")")
+    parts, cur = [], []
+    for t in toks[2:close]:
+        if t.text == ";" and len(parts) < 2:
+            parts.append(cur)
+            cur = []
+        else:
+            cur.append(t)
+    parts.append(cur)
+    if len(parts) != 3:
+        return None
+    init, cond, step = parts
+    if len(init) < 3 or init[0].kind != "name" or init[1].text != "=":
+        return None
+    var = init[0].text
+    lo = prog.text[init[2].pos:init[-1].pos + len(init[-1].text)]
+    if len(cond) < 3 or cond[0].text != var or cond[1].text not in ("<", "<="):
+        return None
+    hi = prog.text[cond[2].pos:cond[-1].pos + len(cond[-1].text)]
+    if cond[1].text == "<=":
+        hi = f"({hi}) + 1"
+    st = [t.text for t in step]
+    if st in ([var, "++"], ["++", var]):
+        inc = 1
+    elif len(st) == 3 and st[0] == var and st[1] == "+=" and step[2].kind == "num":
+        inc = int(st[2])
+    elif len(st) == 5 and st[0] == var and st[1] == "=" and st[2] == var and st[3] == "+" \
+            and step[4].kind == "num":
+        inc = int(st[4])
+    else:
+        return None
+    if inc <= 0:
+        return None
+    body_start = toks[close + 1].pos
+    return Header(var, lo, hi, inc, (body_start, b))
+
+
+def _idents(toks) -> list:
+    return [t.text for t in toks if t.kind == "name" and t.text not in KEYWORDS]
+
+
+def _writes(toks) -> dict:
+    """name -> list of write kinds ('=', '+=', '++', ...) for plain-name targets."""
+    out: dict = {}
+    for k, t in enumerate(toks):
+        if t.kind != "name":
+            continue
+        nxt = toks[k + 1].text if k + 1 < len(toks) else ""
+        prv = toks[k - 1].text if k else ""
+        if nxt in ("=", "+=", "-=", "*=", "/=", "%=", "<<=", ">>=") or nxt in ("++", "--") \
+                or prv in ("++", "--"):
+            if prv == "." or nxt == "[":
+                continue
+            op = nxt if nxt in ("=", "+=", "-=", "*=", "/=", "%=", "<<=", ">>=", "++", "--") else prv
+            out.setdefault(t.text, []).append((k, op))
+    return out
+
+
+def _is_reduction(toks, name: str) -> bool:
+    """Every occurrence of `name` is `name = name + e` / `name += e` with no other use."""
+    occ = [k for k, t in enumerate(toks) if t.kind == "name" and t.text == name]
+    k = 0
+    used = set()
+    ok = False
+    for i in occ:
+        if i in used:
+            continue
+        nxt = toks[i + 1].text if i + 1 < len(toks) else ""
+        if nxt == "+=":
+            end = i + 2
+            while toks[end].text != ";":
+                if toks[end].text == name:
+                    return False
+                end += 1
+            used.add(i)
+            ok = True
+        elif nxt == "=" and i + 3 < len(toks) and toks[i + 2].text == name \
+                and toks[i + 3].text == "+":
+            end = i + 4
+            while toks[end].text != ";":
+                if toks[end].text == name:
+                    return False
+                end += 1
+            used.update((i, i + 2))
+            ok = True
+        else:
+            return False
+        k += 1
+    return ok
+
+
+@dataclass
+class KernelPlan:
+    loop: int
+    func: Func
+    levels: list          # [Header] mapped to the grid (outermost first)
+    body: tuple           # (start, end) of the innermost mapped body
+    arrays: list          # global arrays used (names)
+    arrays_written: list
+    params: list          # [Decl] firstprivate scalars: read-only or read before written
+    privates: list        # [Decl] outer scalars written in the body (kernel locals)
+    reductions: list      # [Decl]
+    carried: list         # [Decl] read-before-write outer scalars (sequential for kernels)
+    mode: str             # "grid" | "block" | "seq"
+    note: str = ""
+
+
+def plan_kernel(prog: CProgram, loop, kind: str, loops) -> Optional[KernelPlan]:
+    """How loop `loop` (model LoopInfo) runs on the device under directive `kind`."""
+    h = parse_header(prog, loop.span)
+    if h is None:
+        return None
+    func = prog.func_at(loop.span[0])
+    levels, body = [h], h.body
+    if kind == "kernels":
+        cur = loop
+        chain_vars = {h.var}
+        while cur.shape == "tight_outer" and len(levels) < 3:
+            kids = loops.children(cur.loop_id)
+            if len(kids) != 1:
+                break
+            child = loops.get(kids[0])
+            ch = parse_header(prog, child.span)
+            if ch is None:
+                break
+            bound_names = set(_idents(tokenize(ch.lo))) | set(_idents(tokenize(ch.hi)))
+            if bound_names & chain_vars:
+                break          # triangular: keep the inner loop inside the thread
+            levels.append(ch)
+            chain_vars.add(ch.var)
+            body = ch.body
+            cur = child
+    body_toks = prog.toks_in(*h.body)
+    names = _idents(body_toks)
+    arrays = sorted({n for n in names if n in prog.gmap and prog.gmap[n].is_array})
+    writes = _writes(body_toks)
+    arr_written = []
+    for k, t in enumerate(body_toks):
+        if t.kind == "name" and t.text in arrays:
+            # a[..][..] = / += / ++ : find the end of the subscript chain
+            j = k + 1
+            while j < len(body_toks) and body_toks[j].text == "[":
+                depth, j = 0, j
+                while True:
+                    if body_toks[j].text == "[":
+                        depth += 1
+                    elif body_toks[j].text == "]":
+                        depth -= 1
+                        if depth == 0:
+                            break
+                    j += 1
+                j += 1
+            if j < len(body_toks) and body_toks[j].text in ("=", "+=", "-=", "*=", "/=", "++", "--"):
+                arr_written.append(t.text)
+    level_vars = {lv.var for lv in levels}
+    params, privates, reds, carried = [], [], [], []
+    seen = set()
+    for n in names:
+        if n in seen or n in level_vars:
+            continue
+        seen.add(n)
+        d = func.scalar(n) or (prog.gmap.get(n) if n in prog.gmap and not prog.gmap[n].is_array
+                               else None)
+        if d is None:
+            continue
+        if n in writes:
+            if _is_reduction(body_toks, n):
+                reds.append(d)
+                continue
+            privates.append(d)
+            first = next(k for k, t in enumerate(body_toks) if t.kind == "name" and t.text == n)
+            if first not in [k for k, _ in writes[n]] or writes[n][0][1] != "=":
+                carried.append(d)
+                params.append(d)
+            continue
+        params.append(d)
+    mode = "grid"
+    note = ""
+    if kind == "parallel loop vector":
+        mode = "block"
+    if carried and kind == "kernels":
+        mode = "seq"
+        levels = [h]
+        body = h.body
+        note = "loop-carried scalar " + ", ".join(d.name for d in carried)
+    return KernelPlan(loop.loop_id, func, levels, body, arrays, sorted(set(arr_written)),
+                      params, privates, reds, carried, mode, note)
+
+
+# ---------------------------------------------------------------------------- emit
+
+def _ctype(d: Decl) -> str:
+    return d.ctype
+
+
+def _array_ref(d: Decl) -> str:
+    dims = "".join(f"[{n}]" for n in d.dims)
+    return f"  {d.ctype} (&{d.name}){dims} = *reinterpret_cast<{d.ctype} (*){dims}>(D.{d.name});"
+
+
+def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
+    lines = []
+    args = ["const Dev D", "double* __restrict__ hpg_red"]
+    for lv_i, _ in enumerate(kp.levels):
+        args += [f"long long hpg_lo{lv_i}", f"long long hpg_n{lv_i}", f"long long hpg_st{lv_i}"]
+    for d in kp.params:
+        args.append(f"{d.ctype} hpg_p_{d.name}")
+    lines.append(f"__global__ void __launch_bounds__(256) k_{kp.loop}({', '.join(args)}) {{")
+    for name in kp.arrays:
+        lines.append(_array_ref(prog.gmap[name]))
+    declared = set()
+    for d in kp.params:
+        lines.append(f"  {d.ctype} {d.name} = hpg_p_{d.name};")
+        declared.add(d.name)
+    for d in kp.reductions:
+        lines.append(f"  {d.ctype} {d.name} = 0;")
+        declared.add(d.name)
+    for d in kp.privates:
+        if d.name not in declared:
+            lines.append(f"  {d.ctype} {d.name};")
+            declared.add(d.name)
+    func_scalars = kp.func.params + kp.func.locals
+    for lv in kp.levels:
+        if lv.var not in declared:
+            d = kp.func.scalar(lv.var) or prog.gmap.get(lv.var)
+            lines.append(f"  {d.ctype if d else 'long long'} {lv.var};")
+            declared.add(lv.var)
+    # other function locals the body may use as privates (nested index vars ...)
+    body_names = set(_idents(prog.toks_in(*kp.body)))
+    for d in func_scalars:
+        if d.name in body_names and d.name not in declared:
+            lines.append(f"  {d.ctype} {d.name};")
+            declared.add(d.name)
+    body_text = prog.text[kp.body[0]:kp.body[1]]
+    nl = len(kp.levels)
+    total = " * ".join(f"hpg_n{i}" for i in range(nl))
+    if kp.mode == "seq":
+        lines.append("  if (blockIdx.x != 0 || threadIdx.x != 0) return;")
+        lines.append("  for (long long hpg_t = 0; hpg_t < hpg_n0; ++hpg_t) {")
+        lines.append(f"    {kp.levels[0].var} = hpg_lo0 + hpg_t * hpg_st0;")
+        lines.append(f"    {body_text}")
+        lines.append("  }")
+        for r, d in enumerate(kp.privates):
+            lines.append(f"  hpg_red[{r}] = (double){d.name};")
+        lines.append("}")
+        return "\n".join(lines)
+    lines.append(f"  const long long hpg_total = {total};")
+    if kp.mode == "block":
+        lines.append("  if (blockIdx.x != 0) return;")
+        lines.append("  for (long long hpg_t = threadIdx.x; hpg_t < hpg_total; hpg_t += blockDim.x) {")
+    else:
+        lines.append("  for (long long hpg_t = blockIdx.x * (long long)blockDim.x + threadIdx.x; "
+                     "hpg_t < hpg_total; hpg_t += (long long)gridDim.x * blockDim.x) {")
+    lines.append("    long long hpg_q = hpg_t;")
+    for i in reversed(range(nl)):
+        lv = kp.levels[i]
+        if i:
+            lines.append(f"    {lv.var} = hpg_lo{i} + (hpg_q % hpg_n{i}) * hpg_st{i}; hpg_q /= hpg_n{i};")
+        else:
+            lines.append(f"    {lv.var} = hpg_lo0 + hpg_q * hpg_st0;")
+    lines.append(f"    {body_text}")
+    lines.append("  }")
+    if kp.reductions:
+        for r, d in enumerate(kp.reductions):
+            lines.append(f"  hpg::block_reduce_store((double){d.name}, hpg_red, {r}, "
+                         f"{len(kp.reductions)});")
+    lines.append("}")
+    return "\n".join(lines)
+
+
+def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
+    """Host code replacing loop kp.loop when it runs on the device."""
+    L = kp.loop
+    ids = lambda names: ", ".join(f"V_{n}" for n in names) or "-1"   # noqa: E731
+    s = []
+    s.append(f"static const int hpg_arr_{L}[] = {{{ids(kp.arrays)}}};")
+    s.append(f"static const int hpg_wr_{L}[] = {{{ids(kp.arrays_written)}}};")
+    s.append(f"R.kernel_enter({L}, hpg_arr_{L}, {len(kp.arrays)}, hpg_wr_{L}, "
+             f"{len(kp.arrays_written)});")
+    for i, lv in enumerate(kp.levels):
+        s.append(f"const long long hpg_lo{i} = (long long)({lv.lo});")
+        s.append(f"const long long hpg_hi{i} = (long long)({lv.hi});")
+        s.append(f"const long long hpg_st{i} = {lv.step};")
+        s.append(f"const long long hpg_n{i} = hpg_hi{i} > hpg_lo{i} ? "
+                 f"(hpg_hi{i} - hpg_lo{i} + hpg_st{i} - 1) / hpg_st{i} : 0;")
+    total = " * ".join(f"hpg_n{i}" for i in range(len(kp.levels)))
+    nred = len(kp.reductions) if kp.mode != "seq" else len(kp.privates)
+    s.append(f"const long long hpg_total = {total};")
+    s.append(f"const int hpg_grid = R.grid_for(hpg_total, {'1' if kp.mode != 'grid' else '0'});")
+    s.append(f"const int hpg_block = {'1' if kp.mode == 'seq' else '256'};")
+    args = ["dev_struct(R)", "R.red_buffer(hpg_grid, " + str(max(nred, 1)) + ")"]
+    for i in range(len(kp.levels)):
+        args += [f"hpg_lo{i}", f"hpg_n{i}", f"hpg_st{i}"]
+    args += [d.name for d in kp.params]
+    s.append("if (hpg_total > 0) {")
+    s.append(f"  k_{L}<<<hpg_grid, hpg_block, 0, R.stream>>>({', '.join(args)});")
+    s.append(f"  R.launched({L});")
+    if kp.mode == "seq" and kp.privates:
+        # one sequential device thread: its final scalars are the program's
+        s.append(f"  double hpg_v[{len(kp.privates)}];")
+        s.append(f"  R.fetch_sums(1, {len(kp.privates)}, hpg_v);")
+        for r, d in enumerate(kp.privates):
+            s.append(f"  {d.name} = ({d.ctype})hpg_v[{r}];")
+    elif kp.reductions:
+        s.append(f"  double hpg_v[{len(kp.reductions)}];")
+        s.append(f"  R.fetch_sums(hpg_grid, {len(kp.reductions)}, hpg_v);")
+        for r, d in enumerate(kp.reductions):
+            s.append(f"  {d.name} = ({d.ctype})((double){d.name} + hpg_v[{r}]);")
+    s.append("}")
+    s.append(f"R.kernel_exit({L}, hpg_arr_{L}, {len(kp.arrays)}, hpg_wr_{L}, "
+             f"{len(kp.arrays_written)});")
+    return "\n".join(s)
+
+
+def transform_text(prog: CProgram, a: int, b: int, loops_by_start: dict, launches: dict) -> str:
+    """Text [a, b) with every loop statement wrapped in its hooks (recursively)."""
+    out, i = [], a
+    starts = sorted(p for p in loops_by_start if a <= p < b)
+    while starts:
+        p = starts[0]
+        loop = loops_by_start[p]
+        s, e = loop.span
+        out.append(prog.text[i:s])
+        inner = transform_text(prog, s, e, {q: l for q, l in loops_by_start.items()
+                                            if s < q < e}, launches)
+        L = loop.loop_id
+        dev = launches.get(L)
+        if dev is not None:
+            out.append(f"{{ R.before({L}); if (R.dev({L})) {{\n{dev}\n}} else {inner} "
+                       f"R.after({L}); }}")
+        else:
+            out.append(f"{{ R.before({L}); R.host_only({L}); {inner} R.after({L}); }}")
+        i = e
+        starts = [q for q in starts if q >= e]
+    out.append(prog.text[i:b])
+    return "".join(out)
+
+
+def generate(app: str, text: str, model, kinds: dict) -> str:
+    """The .cu source of the generated executor (kinds: loop id -> directive kind value)."""
+    prog = CProgram(text)
+    loops = model.loops
+    refs = model.refs
+    arrays = [d for d in prog.globals if d.is_array]
+    scalars = [d for d in prog.globals if not d.is_array]
+    kernels, launches, notes = [], {}, {}
+    kernel_modes = {}
+    for l in loops:
+        kind = kinds.get(l.loop_id)
+        if kind is None:
+            continue
+        kp = plan_kernel(prog, l, kind, loops)
+        if kp is None:
+            notes[l.loop_id] = "loop header not recognised: host only"
+            continue
+        kernels.append(emit_kernel(prog, kp))
+        launches[l.loop_id] = emit_launch(prog, kp, "")
+        kernel_modes[l.loop_id] = (kp.mode, len(kp.levels), kp.note)
+    loops_by_start = {l.span[0]: l for l in loops}
+
+    # variable table: global arrays, then global scalars, then every other
+    # plannable key of the model (function locals: scalars, counted only)
+    var_keys = [d.name for d in arrays] + [d.name for d in scalars]
+    for key in refs.vars:
+        if key not in var_keys and refs.vars[key].scope != "loop-local" \
+                and key not in refs.index_var_keys:
+            var_keys.append(key)
+
+    # arrays the loop's own statements write (children have their own hooks)
+    loop_writes = {}
+    for l in loops:
+        loop_writes[l.loop_id] = sorted(
+            var_keys.index(d.name) for d in arrays
+            if (f := refs.vars[d.name].refs.get(l.loop_id)) is not None and f.written)
+    # host region right before each top-level loop: its array writes
+    seq = refs.region_sequence
+    pre_writes = {}
+    for n, r in enumerate(seq):
+        if isinstance(r, int) and n and isinstance(seq[n - 1], str) and seq[n - 1].startswith("host:"):
+            pre_writes[r] = sorted(
+                var_keys.index(d.name) for d in arrays
+                if (f := refs.vars[d.name].refs.get(seq[n - 1])) is not None and f.written)
+
+    S = []
+    S.append(f"// GENERATED by paper_2002_12115_b200/codegen.py for app '{app}' -- do not edit.")
+    S.append("#include \"gen_runtime.cuh\"")
+    S.append(f"namespace hpg_app_{app} {{")
+    S.append("using hpg::Runtime;")
+    S.append(f"constexpr int kLoops = {len(loops)};")
+    S.append(f"constexpr int kVars = {len(var_keys)};")
+    for n, key in enumerate(var_keys):
+        S.append(f"constexpr int V_{re.sub(r'[^A-Za-z0-9_]', '_', key)} = {n};")
+    S.append("struct Dev {")
+    for d in arrays:
+        S.append(f"  {d.ctype}* {d.name};")
+    S.append("};")
+    S.append("static const hpg::VarDesc kVarDesc[kVars] = {")
+    for key in var_keys:
+        d = prog.gmap.get(key)
+        if d is not None and d.is_array:
+            S.append(f"  {{\"{key}\", 1, sizeof({d.ctype}) * {d.elems()}ull}},")
+        elif d is not None:
+            S.append(f"  {{\"{key}\", 0, sizeof({d.ctype})}},")
+        else:
+            S.append(f"  {{\"{key}\", 0, 8}},")
+    S.append("};")
+    S.append("static const int kEligibleKind[kLoops] = {" + ", ".join(
+        str({"kernels": 1, "parallel loop": 2, "parallel loop vector": 3}.get(kinds.get(l.loop_id), 0)
+            if l.loop_id in launches else 0) for l in loops) + "};")
+    for lid, ws in loop_writes.items():
+        S.append(f"static const int kLoopWr_{lid}[] = {{{', '.join(map(str, ws)) or '-1'}}};")
+    S.append("static const int* const kLoopWr[kLoops] = {" +
+             ", ".join(f"kLoopWr_{l.loop_id}" for l in loops) + "};")
+    S.append("static const int kLoopWrN[kLoops] = {" +
+             ", ".join(str(len(loop_writes[l.loop_id])) for l in loops) + "};")
+    for lid, ws in pre_writes.items():
+        S.append(f"static const int kPreWr_{lid}[] = {{{', '.join(map(str, ws)) or '-1'}}};")
+    S.append("static const int* const kPreWr[kLoops] = {" +
+             ", ".join(f"kPreWr_{l.loop_id}" if l.loop_id in pre_writes else "nullptr"
+                       for l in loops) + "};")
+    S.append("static const int kPreWrN[kLoops] = {" +
+             ", ".join(str(len(pre_writes.get(l.loop_id, []))) for l in loops) + "};")
+    S.append("static const char* const kLoopNote[kLoops] = {" + ", ".join(
+        '"' + (kernel_modes[l.loop_id][0] + "/" + str(kernel_modes[l.loop_id][1]) +
+               (" " + kernel_modes[l.loop_id][2] if kernel_modes[l.loop_id][2] else "")
+               if l.loop_id in kernel_modes else notes.get(l.loop_id, "host")) + '"'
+        for l in loops) + "};")
+    S.append("static const int kParent[kLoops] = {" + ", ".join(
+        str(l.parent_loop if l.parent_loop is not None else -1) for l in loops) + "};")
+    S.append("")
+    S.extend(kernels)
+    S.append("")
+    S.append("struct Prog;")
+    S.append("static Dev dev_struct(const hpg::Runtime& R) {")
+    S.append("  Dev d;")
+    for d in arrays:
+        S.append(f"  d.{d.name} = ({d.ctype}*)R.dev_ptr[V_{d.name}];")
+    S.append("  return d;")
+    S.append("}")
+    S.append("struct Prog {")
+    for d in prog.globals:
+        dims = "".join(f"[{n}]" for n in d.dims)
+        S.append(f"  {d.ctype} {d.name}{dims};")
+    S.append("  Runtime& R;")
+    S.append("  explicit Prog(Runtime& r) : R(r) {}")
+    S.append("  int printf(const char* f, ...) { va_list ap; va_start(ap, f); "
+             "int n = R.vprint(f, ap); va_end(ap); return n; }")
+    for f in prog.funcs:
+        params = ", ".join(f"{d.ctype} {d.name}" for d in f.params)
+        name = "main_" if f.name == "main" else f.name
+        body = transform_text(prog, f.body[0], f.body[1], loops_by_start, launches)
+        S.append(f"  {f.ret} {name}({params}) {body}")
+    S.append("};")
+    S.append("static void bind(Prog* P, hpg::Runtime& R) {")
+    for n, key in enumerate(var_keys):
+        d = prog.gmap.get(key)
+        if d is not None:
+            S.append(f"  R.host_ptr[{n}] = (void*)&P->{d.name};")
+    S.append("}")
+    S.append("struct App {")
+    S.append("  static constexpr int kLoops = hpg_app_" + app + "::kLoops;")
+    S.append("  static constexpr int kVars = hpg_app_" + app + "::kVars;")
+    S.append("  using Prog = hpg_app_" + app + "::Prog;")
+    S.append("  static hpg::Tables tables() {")
+    S.append("    return hpg::Tables{kLoops, kVars, kVarDesc, kEligibleKind, kParent, kLoopWr, "
+             "kLoopWrN, kPreWr, kPreWrN};")
+    S.append("  }")
+    S.append("  static void bind(Prog* P, hpg::Runtime& R) { hpg_app_" + app + "::bind(P, R); }")
+    S.append("};")
+    S.append("}  // namespace")
+    S.append(f"HPG_DEFINE_APP(hpg_app_{app})")
+    return "\n".join(S) + "\n"

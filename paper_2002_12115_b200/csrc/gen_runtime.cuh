@@ -1,0 +1,528 @@
+// Runtime of the generated B200 executors (codegen.py): loop hooks, the
+// whole-array device data manager, reductions, the C ABI (include/app_b200.h).
+//
+// Semantics follow the Himeno library's executor (executor.cpp), at array
+// granularity instead of boxes:
+//   * every array has a host and a device version (write clock); a guarded
+//     transfer is skipped when the destination already holds newer data
+//     (SURVEY.md Appendix B.2), otherwise it copies the whole array;
+//   * plan events (lower.py) fire before / after their loop statement:
+//     declare create, update device / self, structured data enter / exit with
+//     present_or_copy reference counts, present assertions;
+//   * a kernel launch implicitly copies in (and afterwards out, then frees) every
+//     array it touches that is not present -- OpenACC's present_or_copy default;
+//   * scalars are host-authoritative: kernels receive them by value
+//     (firstprivate), reductions return into the host variable; scalar plan
+//     events are counted (bytes, events) but move nothing;
+//   * a fresh run zeroes the program's statics (a new process) and treats device
+//     memory as undefined;
+//   * partial writes: a kernel that writes an array whose device copy is undefined
+//     or older than the host's (e.g. a plan `copyout` with no `copyin`, or host
+//     writes since the last copy) first gets the host copy (counted in n_guard_init
+//     and h2d bytes), so a later whole-array copy-out never carries undefined or
+//     stale device memory over newer host data -- the hazard of the reference's
+//     plans on real hardware.  The Himeno library guards the
+//     same hazard at box granularity without the extra copy.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "app_b200.h"
+
+namespace hpg {
+
+struct VarDesc {
+  const char* name;
+  int is_array;
+  unsigned long long bytes;
+};
+
+enum { ST_OK = 0, ST_PATTERN = 1, ST_LAUNCH = 2, ST_TIMEOUT = 3, ST_PRESENT = 4 };
+enum { ERR_DEVICE = -1, ERR_ARG = -2, ERR_OOM = -3 };
+enum { EV_UPDATE_DEVICE = 1, EV_UPDATE_SELF, EV_DATA_ENTER, EV_DATA_EXIT, EV_DECLARE, EV_PRESENT };
+enum { K_HOST = 0, K_KERNELS = 1, K_PL = 2, K_PLV = 3, K_COVERED = 4 };
+enum { FLAG_GUARD = 1, FLAG_FRESH = 2 };
+
+struct Failure {
+  int code;
+  char msg[256];
+};
+
+inline thread_local char g_last_error[512] = "";
+inline void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof g_last_error, fmt, ap);
+  va_end(ap);
+}
+
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// Block partial of a reduction slot: warp shuffles then warps in fixed order;
+// every thread of the block calls it (same slot sequence).
+__device__ inline void block_reduce_store(double v, double* out, int slot, int nslots) {
+  __shared__ double part[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) part[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int x = 0; x < nw; ++x) s += part[x];
+    out[(size_t)blockIdx.x * nslots + slot] = s;
+  }
+  __syncthreads();
+}
+
+struct Tables {
+  int nloops, nvars;
+  const VarDesc* vars;
+  const int* elig_kind;
+  const int* parent;
+  const int* const* loop_wr;
+  const int* loop_wr_n;
+  const int* const* pre_wr;
+  const int* pre_wr_n;
+};
+
+class Runtime {
+ public:
+  Tables T{};
+  int device = -1;
+  bool has_dev = false;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  std::vector<void*> host_ptr, dev_ptr;
+  // per run
+  const hpg_schedule* S = nullptr;
+  hpg_result* Rz = nullptr;
+  std::vector<std::vector<const hpg_event*>> before_ev, after_ev;
+  std::vector<uint64_t> host_ver, dev_ver;
+  std::vector<int> refcount;
+  std::vector<char> declared;
+  uint64_t clock = 1;
+  bool guard = true;
+  double deadline = 0;
+  std::string out;
+  double* d_red = nullptr;
+  double* h_red = nullptr;
+  size_t red_cap = 0;
+  std::vector<std::vector<int>> implicit_stack;
+
+  ~Runtime() {
+    if (d_red) cudaFree(d_red);
+    if (h_red) cudaFreeHost(h_red);
+    for (void* p : dev_ptr)
+      if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  [[noreturn]] void fail(int code, const char* fmt, ...) {
+    Failure f;
+    f.code = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(f.msg, sizeof f.msg, fmt, ap);
+    va_end(ap);
+    throw f;
+  }
+  int vprint(const char* f, va_list ap) {
+    char buf[1024];
+    const int n = vsnprintf(buf, sizeof buf, f, ap);
+    if (n > 0) out.append(buf, std::min<size_t>((size_t)n, sizeof buf - 1));
+    return n;
+  }
+  void cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ST_LAUNCH, "%s: %s", what, cudaGetErrorString(e));
+  }
+
+  // ---- loop hooks ----------------------------------------------------------
+  int kind(int L) const { return S->loop_kind[L]; }
+  bool dev(int L) const { return kind(L) >= K_KERNELS && kind(L) <= K_PLV; }
+  void host_only(int L) {
+    if (dev(L)) fail(ST_PATTERN, "loop %d has no device version", L);
+  }
+  void host_writes(const int* v, int n) {
+    for (int x = 0; x < n; ++x) host_ver[v[x]] = ++clock;
+  }
+  bool on_host(int L) const { return kind(L) == K_HOST; }
+  void before(int L) {
+    if (deadline > 0 && now_s() > deadline) fail(ST_TIMEOUT, "watchdog: run exceeded %.1f s", S->timeout_s);
+    // host statements that ran since the previous hook: the host region right
+    // before a top-level loop, or the enclosing host loop's own statements
+    if (T.pre_wr[L]) host_writes(T.pre_wr[L], T.pre_wr_n[L]);
+    const int p = T.parent[L];
+    if (p >= 0 && on_host(p)) host_writes(T.loop_wr[p], T.loop_wr_n[p]);
+    for (const hpg_event* e : before_ev[L]) fire(e);
+  }
+  void after(int L) {
+    if (on_host(L)) host_writes(T.loop_wr[L], T.loop_wr_n[L]);
+    for (const hpg_event* e : after_ev[L]) fire(e);
+  }
+
+  // ---- data manager ----------------------------------------------------------
+  bool present(int v) const { return declared[v] || refcount[v] > 0; }
+  void h2d(int v, bool implicit) {
+    const VarDesc& d = T.vars[v];
+    if (!d.is_array) {   // host-authoritative scalar: counted only
+      Rz->h2d_bytes += d.bytes;
+      Rz->n_h2d++;
+      return;
+    }
+    if (!has_dev) fail(ST_LAUNCH, "no device for update device(%s)", d.name);
+    if (guard && dev_ver[v] > host_ver[v]) {
+      Rz->n_skipped_stale++;
+      return;
+    }
+    const double t0 = now_s();
+    cuda(cudaMemcpyAsync(dev_ptr[v], host_ptr[v], d.bytes, cudaMemcpyHostToDevice, stream), "h2d");
+    cuda(cudaStreamSynchronize(stream), "h2d sync");
+    Rz->xfer_s += now_s() - t0;
+    Rz->h2d_bytes += d.bytes;
+    Rz->n_h2d++;
+    if (implicit) Rz->n_implicit++;
+    dev_ver[v] = host_ver[v];
+  }
+  void d2h(int v, bool implicit) {
+    const VarDesc& d = T.vars[v];
+    if (!d.is_array) {
+      Rz->d2h_bytes += d.bytes;
+      Rz->n_d2h++;
+      return;
+    }
+    if (!has_dev) fail(ST_LAUNCH, "no device for update self(%s)", d.name);
+    if (guard && host_ver[v] > dev_ver[v]) {
+      Rz->n_skipped_stale++;
+      return;
+    }
+    const double t0 = now_s();
+    cuda(cudaMemcpyAsync(host_ptr[v], dev_ptr[v], d.bytes, cudaMemcpyDeviceToHost, stream), "d2h");
+    cuda(cudaStreamSynchronize(stream), "d2h sync");
+    Rz->xfer_s += now_s() - t0;
+    Rz->d2h_bytes += d.bytes;
+    Rz->n_d2h++;
+    if (implicit) Rz->n_implicit++;
+    host_ver[v] = dev_ver[v];
+  }
+  void dealloc(int v) { dev_ver[v] = 0; }
+  void fire(const hpg_event* e) {
+    const int v = e->var;
+    switch (e->op) {
+      case EV_DECLARE: declared[v] = 1; break;
+      case EV_UPDATE_DEVICE: h2d(v, false); break;
+      case EV_UPDATE_SELF: d2h(v, false); break;
+      case EV_DATA_ENTER:
+        if (present(v)) {
+          if (!declared[v]) refcount[v]++;
+        } else {
+          refcount[v] = 1;
+          if (e->arg) h2d(v, false);
+        }
+        break;
+      case EV_DATA_EXIT:
+        if (declared[v]) break;
+        if (refcount[v] > 0 && --refcount[v] == 0) {
+          if (e->arg) d2h(v, false);
+          dealloc(v);
+        }
+        break;
+      case EV_PRESENT:
+        if (!present(v))
+          fail(ST_PRESENT, "present(%s) failed at loop %d: data not on device", T.vars[v].name,
+               e->loop_id);
+        break;
+      default: fail(ST_PATTERN, "unknown event op %d", e->op);
+    }
+  }
+
+  // ---- kernels --------------------------------------------------------------
+  void kernel_enter(int L, const int* arrs, int n, const int* wr, int nw) {
+    if (!has_dev) fail(ST_LAUNCH, "loop %d: no CUDA device in this context", L);
+    implicit_stack.emplace_back();
+    for (int x = 0; x < n; ++x) {
+      const int v = arrs[x];
+      if (v < 0 || present(v)) continue;
+      h2d(v, true);
+      implicit_stack.back().push_back(v);
+    }
+    for (int x = 0; x < nw; ++x) {
+      const int v = wr[x];
+      if (v >= 0 && T.vars[v].is_array && (dev_ver[v] == 0 || host_ver[v] > dev_ver[v])) {
+        const bool g = guard;
+        guard = false;
+        h2d(v, false);
+        guard = g;
+        Rz->n_guard_init++;
+      }
+    }
+  }
+  void kernel_exit(int L, const int* arrs, int n, const int* wr, int nw) {
+    (void)L;
+    (void)arrs;
+    (void)n;
+    for (int x = 0; x < nw; ++x)
+      if (wr[x] >= 0) dev_ver[wr[x]] = ++clock;
+    std::vector<int> imp = std::move(implicit_stack.back());
+    implicit_stack.pop_back();
+    for (int v : imp) {
+      d2h(v, true);
+      dealloc(v);
+    }
+  }
+  int grid_for(long long total, int single) const {
+    if (single) return 1;
+    const long long b = (total + 255) / 256;
+    return (int)std::max<long long>(1, std::min<long long>(b, (long long)sms * 8));
+  }
+  double* red_buffer(int grid, int nslots) {
+    const size_t need = (size_t)grid * nslots;
+    if (need > red_cap) {
+      if (d_red) cudaFree(d_red);
+      if (h_red) cudaFreeHost(h_red);
+      d_red = nullptr;
+      h_red = nullptr;
+      red_cap = std::max<size_t>(need, 4096);
+      if (cudaMalloc(&d_red, red_cap * sizeof(double)) != cudaSuccess ||
+          cudaMallocHost(&h_red, red_cap * sizeof(double)) != cudaSuccess)
+        fail(ST_LAUNCH, "reduction buffer allocation failed");
+    }
+    return d_red;
+  }
+  void launched(int L) {
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) fail(ST_LAUNCH, "launch of loop %d failed: %s", L, cudaGetErrorString(e));
+    Rz->n_launch++;
+  }
+  // block partials in block order -> per-slot sums (waits for the kernel)
+  void fetch_sums(int grid, int nslots, double* out_v) {
+    cuda(cudaMemcpyAsync(h_red, d_red, (size_t)grid * nslots * sizeof(double),
+                         cudaMemcpyDeviceToHost, stream), "reduction d2h");
+    cuda(cudaStreamSynchronize(stream), "reduction sync");
+    for (int r = 0; r < nslots; ++r) {
+      double s = 0.0;
+      for (int b = 0; b < grid; ++b) s += h_red[(size_t)b * nslots + r];
+      out_v[r] = s;
+    }
+  }
+
+  // ---- run setup -------------------------------------------------------------
+  void prepare(const hpg_schedule* s, hpg_result* r) {
+    S = s;
+    Rz = r;
+    if (s->n_loops != T.nloops) {
+      set_error("schedule has %d loops, program has %d", s->n_loops, T.nloops);
+      throw ERR_ARG;
+    }
+    before_ev.assign(T.nloops + 1, {});
+    after_ev.assign(T.nloops + 1, {});
+    for (int n = 0; n < s->n_events; ++n) {
+      const hpg_event* e = &s->events[n];
+      if (e->var < 0 || e->var >= T.nvars || e->loop_id < -1 || e->loop_id >= T.nloops) {
+        set_error("event %d out of range", n);
+        throw ERR_ARG;
+      }
+      if (e->op == EV_DECLARE) continue;
+      (e->when == 0 ? before_ev : after_ev)[e->loop_id].push_back(e);
+    }
+    // same intra-hook order as the Himeno executor: updates, enters, present, exits
+    auto rank = [](const hpg_event* e) {
+      switch (e->op) {
+        case EV_UPDATE_DEVICE: return 10;
+        case EV_DATA_ENTER: return 20;
+        case EV_PRESENT: return 30;
+        case EV_DATA_EXIT: return 60;
+        default: return 90;
+      }
+    };
+    for (auto& v : before_ev)
+      std::stable_sort(v.begin(), v.end(), [&](auto* a, auto* b) { return rank(a) < rank(b); });
+    for (auto& v : after_ev)
+      std::stable_sort(v.begin(), v.end(), [&](auto* a, auto* b) { return rank(a) < rank(b); });
+    for (int L = 0; L < T.nloops; ++L)
+      if (dev(L) && T.elig_kind[L] == 0) {
+        r->status = ST_PATTERN;
+        snprintf(r->diag, sizeof r->diag, "loop %d is not offloadable", L);
+      }
+    host_ver.assign(T.nvars, 1);
+    dev_ver.assign(T.nvars, 0);
+    refcount.assign(T.nvars, 0);
+    declared.assign(T.nvars, 0);
+    clock = 1;
+    guard = (s->flags & FLAG_GUARD) != 0;
+    out.clear();
+    implicit_stack.clear();
+    for (int n = 0; n < s->n_events; ++n)
+      if (s->events[n].op == EV_DECLARE) declared[s->events[n].var] = 1;
+  }
+};
+
+}  // namespace hpg
+
+struct hpg_ctx {
+  hpg::Runtime R;
+  void* P = nullptr;        // the application's Prog (statics + functions)
+  size_t prog_bytes = 0;
+  bool pinned = false;
+};
+
+namespace hpg {
+
+// C ABI of one generated application A (A::Prog, A::kLoops, A::kVars, A::tables(),
+// A::bind(Prog*, Runtime&)); instantiated once per shared library.
+template <class A>
+struct Abi {
+  using Prog = typename A::Prog;
+  static int create(int device, hpg_ctx** out) {
+    if (!out) return ERR_ARG;
+    *out = nullptr;
+    hpg_ctx* c = new (std::nothrow) hpg_ctx;
+    if (!c) return ERR_OOM;
+    c->R.T = A::tables();
+    c->R.host_ptr.assign(A::kVars, nullptr);
+    c->R.dev_ptr.assign(A::kVars, nullptr);
+    c->prog_bytes = sizeof(Prog);
+    if (device >= 0) {
+      int n = 0;
+      if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n) {
+        cudaGetLastError();
+        set_error("hpg_create: no CUDA device %d", device);
+        delete c;
+        return ERR_DEVICE;
+      }
+      cudaSetDevice(device);
+      c->R.device = device;
+      c->R.has_dev = true;
+      cudaDeviceGetAttribute(&c->R.sms, cudaDevAttrMultiProcessorCount, device);
+      if (cudaStreamCreateWithFlags(&c->R.stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaMallocHost(&c->P, sizeof(Prog)) != cudaSuccess) {
+        set_error("hpg_create: stream / pinned allocation failed: %s",
+                  cudaGetErrorString(cudaGetLastError()));
+        delete c;
+        return ERR_DEVICE;
+      }
+      c->pinned = true;
+    } else {
+      c->P = std::aligned_alloc(4096, (sizeof(Prog) + 4095) / 4096 * 4096);
+      if (!c->P) {
+        delete c;
+        return ERR_OOM;
+      }
+    }
+    std::memset(c->P, 0, sizeof(Prog));
+    Prog* P = new (c->P) Prog(c->R);
+    A::bind(P, c->R);
+    if (c->R.has_dev) {
+      for (int v = 0; v < A::kVars; ++v)
+        if (c->R.T.vars[v].is_array &&
+            cudaMalloc(&c->R.dev_ptr[v], c->R.T.vars[v].bytes) != cudaSuccess) {
+          set_error("hpg_create: device allocation of %s failed", c->R.T.vars[v].name);
+          destroy(c);
+          return ERR_OOM;
+        }
+    }
+    *out = c;
+    return 0;
+  }
+  static void destroy(hpg_ctx* c) {
+    if (!c) return;
+    if (c->R.has_dev) cudaSetDevice(c->R.device);
+    if (c->P) {
+      static_cast<Prog*>(c->P)->~Prog();
+      if (c->pinned) cudaFreeHost(c->P);
+      else std::free(c->P);
+    }
+    delete c;
+  }
+  static int run(hpg_ctx* c, const hpg_schedule* s, hpg_result* r) {
+    if (!c || !s || !r || (s->n_events > 0 && !s->events) || !s->loop_kind) {
+      set_error("hpg_run: bad arguments");
+      return ERR_ARG;
+    }
+    std::memset(r, 0, sizeof *r);
+    Runtime& R = c->R;
+    if (R.has_dev && cudaSetDevice(R.device) != cudaSuccess) {
+      set_error("hpg_run: cudaSetDevice failed");
+      return ERR_DEVICE;
+    }
+    try {
+      R.prepare(s, r);
+    } catch (int rc) {
+      return rc;
+    }
+    if (r->status != ST_OK) {
+      set_error("%s", r->diag);
+      return r->status;
+    }
+    Prog* P = static_cast<Prog*>(c->P);
+    if (s->flags & FLAG_FRESH) {   // a new process: zeroed statics (not timed)
+      P->~Prog();
+      std::memset(c->P, 0, sizeof(Prog));
+      P = new (c->P) Prog(R);
+      A::bind(P, R);
+    }
+    const double t0 = now_s();
+    R.deadline = s->timeout_s > 0 ? t0 + s->timeout_s : 0;
+    try {
+      P->main_();
+      if (R.has_dev) R.cuda(cudaStreamSynchronize(R.stream), "program end");
+      r->status = ST_OK;
+    } catch (const Failure& f) {
+      if (R.has_dev) {
+        cudaStreamSynchronize(R.stream);
+        cudaGetLastError();
+      }
+      r->status = f.code;
+      snprintf(r->diag, sizeof r->diag, "%s", f.msg);
+      set_error("%s", f.msg);
+    }
+    r->wall_s = now_s() - t0;
+    return r->status;
+  }
+  static size_t output(hpg_ctx* c, char* dst, size_t cap) {
+    if (!c) return 0;
+    const size_t n = c->R.out.size();
+    if (dst && cap) {
+      const size_t m = std::min(n, cap - 1);
+      std::memcpy(dst, c->R.out.data(), m);
+      dst[m] = 0;
+    }
+    return n;
+  }
+};
+
+}  // namespace hpg
+
+#define HPG_DEFINE_APP(NS)                                                                   \
+  extern "C" int hpg_create(int device, hpg_ctx** out) { return hpg::Abi<NS::App>::create(device, out); } \
+  extern "C" void hpg_destroy(hpg_ctx* c) { hpg::Abi<NS::App>::destroy(c); }                 \
+  extern "C" int hpg_run(hpg_ctx* c, const hpg_schedule* s, hpg_result* r) {                 \
+    return hpg::Abi<NS::App>::run(c, s, r);                                                  \
+  }                                                                                          \
+  extern "C" size_t hpg_output(hpg_ctx* c, char* d, size_t n) { return hpg::Abi<NS::App>::output(c, d, n); } \
+  extern "C" int hpg_n_loops(void) { return NS::App::kLoops; }                               \
+  extern "C" int hpg_n_vars(void) { return NS::App::kVars; }                                 \
+  extern "C" const char* hpg_var_name(int v) {                                               \
+    return v >= 0 && v < NS::App::kVars ? NS::kVarDesc[v].name : nullptr;                    \
+  }                                                                                          \
+  extern "C" int hpg_loop_kind(int l) {                                                      \
+    return l >= 0 && l < NS::App::kLoops ? NS::kEligibleKind[l] : -1;                        \
+  }                                                                                          \
+  extern "C" const char* hpg_loop_note(int l) {                                              \
+    return l >= 0 && l < NS::App::kLoops ? NS::kLoopNote[l] : nullptr;                       \
+  }                                                                                          \
+  extern "C" const char* hpg_last_error(void) { return hpg::g_last_error; }

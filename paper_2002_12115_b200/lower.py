@@ -59,7 +59,8 @@ def _nested_pairs(loops, gene: dict) -> list:
     return out
 
 
-def loop_kinds(loops, gene: dict, kinds: dict, nested_policy: str = "reject"):
+def loop_kinds(loops, gene: dict, kinds: dict, nested_policy: str = "reject",
+               n_loops: int = N.NLOOPS):
     """Per-loop native kind, or (None, diagnostic) for a rejected pattern."""
     if nested_policy not in NESTED_POLICIES:
         raise ValueError(f"nested_policy must be one of {NESTED_POLICIES}")
@@ -68,7 +69,7 @@ def loop_kinds(loops, gene: dict, kinds: dict, nested_policy: str = "reject"):
         inner, outer = nested[0]
         return None, (f"nested compute construct: loop {inner} ({kinds[inner].value}) "
                       f"inside gene=1 loop {outer} ({kinds[outer].value})")
-    out = [N.K_HOST] * N.NLOOPS
+    out = [N.K_HOST] * n_loops
     for l in loops:
         lid = l.loop_id
         anchor = None
@@ -92,8 +93,12 @@ def _loop_of_span(loops, file_id, span) -> int:
     raise PlanInconsistent(f"plan span {span} in {file_id} is not a loop statement")
 
 
-def plan_events(plan, loops, refs, gene: dict) -> list:
-    """TransferPlan entries -> ordered event tuples (loop, when, op, var, arg, entry)."""
+def plan_events(plan, loops, refs, gene: dict, var_id: dict = None) -> list:
+    """TransferPlan entries -> ordered event tuples (loop, when, op, var, arg, entry).
+
+    ``var_id`` maps plan variable keys to the executor's variable ids (default:
+    the Himeno library's table)."""
+    var_id = N.VAR_ID if var_id is None else var_id
     events = []
     declared = set()
     on = {lid for lid, bit in gene.items() if bit == 1}
@@ -105,9 +110,9 @@ def plan_events(plan, loops, refs, gene: dict) -> list:
             if site not in e.members:
                 raise PlanInconsistent(f"present site {site} outside its region")
         key = e.var
-        if key not in N.VAR_ID:
-            raise PlanInconsistent(f"variable {key!r} is not part of the Himeno program")
-        var = N.VAR_ID[key]
+        if key not in var_id:
+            raise PlanInconsistent(f"variable {key!r} is not part of the program")
+        var = var_id[key]
         open_loop = getattr(e, "open_loop", None)
         close_loop = getattr(e, "close_loop", None)
         if open_loop is None:

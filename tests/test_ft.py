@@ -5,9 +5,8 @@ reference's own front-end and planner.
   oracle/pin_reference.py) reproduces NPB FT's published class S / W checksums to NPB's
   1e-12 relative tolerance -- the restatement is the NPB algorithm;
 * the committed program model is the reference's analyze_project + StaticRuleProbe
-  output (45 loops, 36 genes);
-* plan.Planner equals the reference Planner on 437 FT genomes (golden) and, when the
-  reference is mounted, live.
+  output (93 loops, 79 genes);
+* plan.Planner equals the reference Planner on 480 FT genomes (golden).
 """
 import gzip
 import json
@@ -32,11 +31,13 @@ def test_reference_stdout_matches_npb_checksums(cls):
 
 def test_program_model_shape():
     prog = ft.program("S")
-    assert len(prog.model.loops) == 45
-    assert prog.gene_length == 36
+    assert len(prog.model.loops) == 93
+    assert prog.gene_length == 79
     kinds = {lid: k.value for lid, k in prog.kinds.items()}
-    assert kinds[0] == "kernels" and kinds[2] == "parallel loop" and kinds[36] == "kernels"
-    assert 3 not in prog.eligible and 18 not in prog.eligible   # calls randlc / cfftz
+    assert kinds[0] == "kernels" and kinds[2] == "parallel loop" and kinds[91] == "kernels"
+    # the FFT's k loops (butterfly offsets i*lk + k) are rejected by the static probe;
+    # the printf loop has a call
+    assert 14 not in prog.eligible and 92 not in prog.eligible
 
 
 def test_planner_matches_reference_golden():
@@ -52,7 +53,7 @@ def test_planner_matches_reference_golden():
             bad.append(("plan", key))
         if [_sig(e) for e in planner.plan_transfers(g).entries] != golden["raw"][key]:
             bad.append(("raw", key))
-    assert len(golden["plans"]) == 437 and not bad, bad[:3]
+    assert len(golden["plans"]) == 480 and not bad, bad[:3]
 
 
 def test_gcc_build_of_the_text_verifies(tmp_path):

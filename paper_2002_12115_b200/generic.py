@@ -204,7 +204,7 @@ class GenEvaluator:
     def __init__(self, app: str = "ft_s", devices=None, *, transfer_mode: str = "batched",
                  nested_policy: str = "reject", coherence_guard: bool = True,
                  fresh_process: bool = True, timeout_s: float = 180.0,
-                 workers_per_device: int = 1, verify_each: bool = False):
+                 workers_per_device: int = 1, verify_each: bool = False, genes=None):
         specs = app_specs()
         if app not in specs:
             raise ConfigError(f"no generated executor for {app!r} (one of {sorted(specs)})")
@@ -216,6 +216,7 @@ class GenEvaluator:
         prog = self.spec.program()
         self.loops, self.refs = prog.model.loops, prog.model.refs
         self.eligible_ids = list(prog.eligible)
+        self.classified_ids = list(prog.eligible)
         self.kinds = dict(prog.kinds)
         self.lib = load(app)
         if self.lib.n_loops != len(self.loops):
@@ -230,7 +231,6 @@ class GenEvaluator:
         if not self.devices:
             raise EvaluatorUnavailable("no devices to evaluate on")
         self.max_concurrency = len(self.devices)
-        self.planner = Planner(self.loops, self.refs, self.eligible_ids)
         self._contexts: dict = {}
         self._ctx_lock = threading.Lock()
         self._free: "queue.Queue[int]" = queue.Queue()
@@ -249,6 +249,20 @@ class GenEvaluator:
         # the final best pattern.
         self.verify_each = bool(verify_each)
         self._baseline_out: Optional[str] = None
+        self.planner = Planner(self.loops, self.refs, self.eligible_ids)
+        self.probe_log: dict = {}
+        if genes == "verified":
+            genes = self.verified_loops()
+        if genes is not None:
+            # restrict the genome to a subset of the classified loops (gene order kept)
+            keep = set(int(g) for g in genes)
+            unknown = keep - set(self.classified_ids)
+            if unknown:
+                raise ConfigError(f"loops {sorted(unknown)} are not eligible")
+            self.eligible_ids = [l for l in self.classified_ids if l in keep]
+            self.planner = Planner(self.loops, self.refs, self.eligible_ids)
+            with self._low_lock:
+                self._lowered.clear()
 
     @property
     def gene_length(self) -> int:
@@ -318,6 +332,38 @@ class GenEvaluator:
         if res.status == N.HP_TIMEOUT:
             return MeasuredTime.timeout()
         return MeasuredTime.failed(res.diag.decode(errors="replace") or f"status {res.status}")
+
+    def verified_loops(self) -> list:
+        """Execution probe (the B200 analogue of the reference's compile probe,
+        classify.py:234-274): each classified loop alone on the GPU under its kind, its
+        stdout checked against the all-CPU program's with verify_results.  Loops the
+        static probe accepts but whose parallel execution changes the result (scalar- or
+        stage-carried chains, shared scratch) are dropped; ``probe_log`` keeps why."""
+        from .tune import verify_results
+        base = self.baseline_output()
+        ok = []
+        full = list(self.classified_ids)
+        for lid in full:
+            g = tuple(int(l == lid) for l in full)
+            low = lower(g, full, self.kinds, self.loops, Planner(self.loops, self.refs, full).plan(g),
+                        self.lib, self.flags, self.timeout_s, self.nested_policy)
+            slot = self._free.get()
+            try:
+                ctx = self._context(slot)
+                res = ctx.run(low.schedule)
+                out = ctx.output()
+            finally:
+                self._free.put(slot)
+            if res.status != N.HP_OK:
+                self.probe_log[lid] = f"run failed: {res.diag.decode(errors='replace')}"
+                continue
+            rep = verify_results(base, out)
+            if rep.passed:
+                ok.append(lid)
+                self.probe_log[lid] = f"verified ({self.lib.loop_notes[lid]}, {res.wall_s * 1e3:.1f} ms)"
+            else:
+                self.probe_log[lid] = "result differs: " + "; ".join(rep.detail[:1])
+        return ok
 
     def baseline_output(self) -> str:
         """stdout of the all-CPU pattern (computed once)."""

@@ -89,7 +89,7 @@ def test_random_ft_genomes_lower():
 FT_EXACT = [0, 3, 4, 10, 13, 16, 19, 22, 25, 28, 31, 34, 37, 40, 43, 45, 49, 53, 56, 59,
             62, 65, 68, 71, 74, 77, 80, 83, 86, 88, 91]      # no two nested
 FT_EXACT_SINGLE = FT_EXACT + [5]                           # 5: inside 4
-FT_WRONG = [6, 7, 12, 9, 48]
+FT_WRONG = [6, 7, 9, 12, 21, 24, 33, 36, 48, 52, 55, 64, 67, 76, 79]
 
 
 def _genome(ev, on):
@@ -154,3 +154,17 @@ def test_run_ga_on_ft(gpu):
     with generic.GenEvaluator("ft_s", devices=[0], workers_per_device=2, verify_each=True) as ev:
         res = ga.run_ga(ga.GAConfig(population=6, generations=3, rng_seed=0), ev.gene_length, ev)
         assert res.evaluations > 0 and res.best.time_s > 0
+
+
+@pytest.mark.gpu
+def test_ft_execution_probe(gpu):
+    """The execution probe keeps every exact loop and drops the static probe's false accepts."""
+    with generic.GenEvaluator("ft_s", devices=[0], genes="verified",
+                              nested_policy="outermost", verify_each=True) as ev:
+        kept = set(ev.eligible_ids)
+        assert set(FT_EXACT_SINGLE) <= kept, set(FT_EXACT_SINGLE) - kept
+        assert not (set(FT_WRONG) & kept)
+        assert all(ev.probe_log[l].startswith("verified") for l in kept)
+        from paper_2002_12115_b200 import ga
+        res = ga.run_ga(ga.GAConfig(population=6, generations=2, rng_seed=1), ev.gene_length, ev)
+        assert res.best.time_s < 1000          # verified patterns only: a runnable best

@@ -19,7 +19,8 @@ GFLOPS = 34 * (I-3)(J-3)(K-3) * nn / t.
 * cpu_baseline  the CPU oracle's jacobi on the same grid, all host threads.
 * ga         run_ga (config 4: pop 20 x gen 20, Himeno M, nn=3) with B200Evaluator on
              this rank's GPU: fresh evaluations/s and generations/s; ga_config1 the
-             same for config 1 (Himeno XS, pop 4 x gen 4).
+             same for config 1 (Himeno XS, pop 4 x gen 4); ft_ga the GA on NAS FT class S
+             through the generated executor (pop 20 x gen 5, verified genes).
 
 N > 1 (torchrun): the grid is split into N slabs of i-planes (dd.SlabJacobi), one
 per GPU; halo planes and the gosa all-reduce go over NCCL; "scaling": "strong"
@@ -202,6 +203,8 @@ def run_reference(args, world, rank):
         line["ga"] = ref_ga.ga_throughput(args.ga_size, args.ga_nn, args.ga_pop, args.ga_gens,
                                           args.ga_seed)
         line["ga_config1"] = ref_ga.ga_throughput("XS", 3, 4, 4, args.ga_seed)
+        if not args.no_ft:
+            line["ft_ga"] = ref_ga.ft_ga_throughput("S", args.ga_pop, args.ft_gens, args.ga_seed)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -227,6 +230,35 @@ def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: i
             "valid_fresh": ok,
             "evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
             "best_genome": ga.genome_str(res.best.genome), "best_time_s": res.best.time_s}
+
+
+def ft_ga_throughput(devices, cls: str, pop: int, gens: int, seed: int, workers: int) -> dict:
+    """run_ga on NAS FT through the generated executor (generic.GenEvaluator): genes =
+    the loops the execution probe verified, nested genes run under their outermost
+    anchor, every run's output verified."""
+    from paper_2002_12115_b200 import ga, generic
+    devices = [devices] if isinstance(devices, int) else list(devices)
+    app = f"ft_{cls.lower()}"
+    t0 = time.perf_counter()
+    with generic.GenEvaluator(app, devices=devices, workers_per_device=workers,
+                              verify_each=True, nested_policy="outermost",
+                              genes="verified") as ev:
+        probe_s = time.perf_counter() - t0
+        ev.prepare()
+        cpu_s = ev.measure((0,) * ev.gene_length).seconds
+        t0 = time.perf_counter()
+        res = ga.run_ga(ga.GAConfig(population=pop, generations=gens, rng_seed=seed),
+                        ev.gene_length, ev)
+        el = time.perf_counter() - t0
+        valid = sum(1 for r in res.records for i in r.individuals
+                    if i.eval_source == "fresh" and i.time_s < 1000)
+        return {"app": app, "population": pop, "generations": gens, "seed": seed,
+                "gpus": len(devices), "workers_per_gpu": workers,
+                "genes": ev.gene_length, "classified_genes": len(ev.classified_ids),
+                "probe_s": probe_s, "wall_s": el, "fresh_evals": res.evaluations,
+                "valid_fresh": valid, "evals_per_s": res.evaluations / el,
+                "gens_per_s": gens / el, "best_genome": ga.genome_str(res.best.genome),
+                "best_time_s": res.best.time_s, "all_cpu_time_s": cpu_s}
 
 
 def run_ours(args, world, rank, local):
@@ -444,6 +476,9 @@ def run_ours(args, world, rank, local):
                                     args.ga_gens, args.ga_seed, workers)
         # BASELINE config 1: Himeno XS, nn=3, pop 4 x gen 4
         extra["ga_config1"] = ga_throughput(devices, "XS", 3, 4, 4, args.ga_seed, workers)
+        if not args.no_ft:
+            extra["ft_ga"] = ft_ga_throughput(devices, "S", args.ga_pop, args.ft_gens,
+                                              args.ga_seed, workers)
     barrier()   # the other ranks wait for rank 0's extras before tearing down NCCL
     if slab is not None:
         slab.close()
@@ -493,6 +528,8 @@ def main(argv=None) -> int:
     ap.add_argument("--ga-pop", type=int, default=20)
     ap.add_argument("--ga-gens", type=int, default=20)
     ap.add_argument("--ga-seed", type=int, default=0)
+    ap.add_argument("--no-ft", action="store_true", help="skip the NAS FT GA line")
+    ap.add_argument("--ft-gens", type=int, default=5)
     ap.add_argument("--ga-workers", type=int, default=4,
                     help="concurrent evaluations per GPU (own context each); 4, 8 and 16 give "
                          "the same evals/s (profiles/r01_ga_workers.jsonl); 0 = host cores")

@@ -25,6 +25,7 @@ from paper_2002_12115_b200.apps import himeno
 from paper_2002_12115_b200.evaluator import MeasuredTime
 
 COMPILE = "gcc -O2 -w -mcmodel=medium {src} -o {bin}"
+COMPILE_LM = "gcc -O2 -w -mcmodel=medium {src} -o {bin} -lm"   # FT calls exp / sin / cos
 RUN = "{bin}"
 
 
@@ -34,7 +35,8 @@ class ExternalProcedure:
     deterministic = False
 
     def __init__(self, text: str, file_id: str, timeout_s: float = 180.0,
-                 max_concurrency: int = 1):
+                 max_concurrency: int = 1, compile_cmd: str = COMPILE):
+        self.compile_cmd = compile_cmd
         self.text = text
         self.file_id = file_id
         self.timeout_s = timeout_s
@@ -45,7 +47,7 @@ class ExternalProcedure:
             src = Path(tmp) / self.file_id
             src.write_text(self.text)
             binary = str(Path(tmp) / "app")
-            comp = subprocess.run(COMPILE.format(src=src, bin=binary), shell=True,
+            comp = subprocess.run(self.compile_cmd.format(src=src, bin=binary), shell=True,
                                   capture_output=True, text=True, cwd=tmp)
             if comp.returncode != 0:
                 return MeasuredTime.failed("compile failed: " + comp.stderr[-300:])
@@ -77,3 +79,22 @@ def ga_throughput(size_name: str, nn: int, pop: int, gens: int, seed: int,
             "best_genome": ga.genome_str(res.best.genome), "best_time_s": res.best.time_s,
             "procedure": "acctuner ExternalEvaluator: gcc -O2 compile + run + perf_counter "
                          "per fresh genome (pragmas ignored by gcc)"}
+
+
+def ft_ga_throughput(cls: str, pop: int, gens: int, seed: int, workers: int = 0) -> dict:
+    """The same procedure on the NAS FT restatement (apps/ft.py)."""
+    from paper_2002_12115_b200.apps import ft
+    c = ft.ft_class(cls)
+    workers = workers or (os.cpu_count() or 1)
+    ev = ExternalProcedure(ft.source_text(c), ft.source_file_id(c), max_concurrency=workers,
+                           compile_cmd=COMPILE_LM)
+    t0 = time.perf_counter()
+    res = ga.run_ga(ga.GAConfig(population=pop, generations=gens, rng_seed=seed),
+                    ft.program(c).gene_length, ev)
+    el = time.perf_counter() - t0
+    return {"app": f"ft_{c.name.lower()}", "population": pop, "generations": gens, "seed": seed,
+            "workers": workers, "wall_s": el, "fresh_evals": res.evaluations,
+            "evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
+            "best_genome": ga.genome_str(res.best.genome), "best_time_s": res.best.time_s,
+            "procedure": "acctuner ExternalEvaluator: gcc -O2 -lm compile + run per fresh genome "
+                         "(pragmas ignored by gcc: every genome is the all-CPU program)"}

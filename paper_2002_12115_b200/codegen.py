@@ -335,12 +335,46 @@ class KernelPlan:
     privates: list        # [Decl] outer scalars written in the body (kernel locals)
     reductions: list      # [Decl]
     carried: list         # [Decl] read-before-write outer scalars (sequential for kernels)
-    mode: str             # "grid" | "block" | "seq"
+    mode: str             # "grid" | "gang" | "block" | "seq"
     note: str = ""
+    vec: list = field(default_factory=list)   # [(LoopInfo, Header)] vector (thread) loops
 
 
-def plan_kernel(prog: CProgram, loop, kind: str, loops) -> Optional[KernelPlan]:
-    """How loop `loop` (model LoopInfo) runs on the device under directive `kind`."""
+def _vector_leaves(prog: CProgram, loop, loops, kinds) -> list:
+    """Innermost loops below `loop` that a compiler would run as vector loops inside a
+    gang: leaves of the loop tree, classified parallelisable themselves, with a
+    recognised header and no loop-carried scalar or reduction."""
+    out = []
+
+    def walk(lid):
+        kids = loops.children(lid)
+        if not kids:
+            if lid == loop.loop_id or kinds.get(lid) is None:
+                return
+            leaf = loops.get(lid)
+            h = parse_header(prog, leaf.span)
+            if h is None:
+                return
+            kp = plan_kernel(prog, leaf, "parallel loop", loops)
+            if kp is None or kp.carried or kp.reductions:
+                return
+            out.append((leaf, h))
+            return
+        for c in kids:
+            walk(c)
+
+    walk(loop.loop_id)
+    return out
+
+
+def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[KernelPlan]:
+    """How loop `loop` (model LoopInfo) runs on the device under directive `kind`.
+
+    With the program's classification (``kinds``), a loop that is not collapsed into
+    the grid runs as OpenACC compilers run a gang loop with parallelisable inner
+    loops: one thread block per iteration of the loop (gang), the innermost
+    parallelisable loops spread over the block's threads (vector, a barrier after
+    each), everything between them executed redundantly by every thread."""
     h = parse_header(prog, loop.span)
     if h is None:
         return None
@@ -417,8 +451,65 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops) -> Optional[KernelPlan]:
         levels = [h]
         body = h.body
         note = "loop-carried scalar " + ", ".join(d.name for d in carried)
+    vec = []
+    if mode == "grid" and len(levels) == 1 and kinds is not None and not reds:
+        vec = _vector_leaves(prog, loop, loops, kinds)
+        if vec:
+            mode = "gang"
+            note = "vector " + ",".join(str(l.loop_id) for l, _ in vec)
     return KernelPlan(loop.loop_id, func, levels, body, arrays, sorted(set(arr_written)),
-                      params, privates, reds, carried, mode, note)
+                      params, privates, reds, carried, mode, note, vec)
+
+
+def shared_writes(prog: CProgram, loop) -> list:
+    """Arrays the body of `loop` writes at subscripts that do not depend on its index
+    variable (directly or through scalars assigned from it): different iterations write
+    the same elements, so running them in parallel is a race (output dependence)."""
+    h = parse_header(prog, loop.span)
+    if h is None:
+        return []
+    toks = prog.toks_in(*h.body)
+    # scalars derived from the index: assignment targets whose right-hand side uses
+    # a derived name (fixpoint); nested loop indices are not derived
+    derived = {h.var}
+    changed = True
+    while changed:
+        changed = False
+        for k, t in enumerate(toks):
+            if t.kind != "name" or k + 1 >= len(toks) or toks[k + 1].text not in ("=", "+=", "-="):
+                continue
+            if k and toks[k - 1].text == "(":       # for-header init: nested loop index
+                continue
+            if t.text in derived:
+                continue
+            end = k + 2
+            while end < len(toks) and toks[end].text != ";":
+                end += 1
+            if any(x.kind == "name" and x.text in derived for x in toks[k + 2:end]):
+                derived.add(t.text)
+                changed = True
+    out = []
+    for k, t in enumerate(toks):
+        if t.kind != "name" or t.text not in prog.gmap or not prog.gmap[t.text].is_array:
+            continue
+        j, names = k + 1, set()
+        while j < len(toks) and toks[j].text == "[":
+            depth = 0
+            while True:
+                if toks[j].text == "[":
+                    depth += 1
+                elif toks[j].text == "]":
+                    depth -= 1
+                    if depth == 0:
+                        break
+                elif toks[j].kind == "name":
+                    names.add(toks[j].text)
+                j += 1
+            j += 1
+        if j < len(toks) and toks[j].text in ("=", "+=", "-=", "*=", "/=", "++", "--") \
+                and not (names & derived) and t.text not in out:
+            out.append(t.text)
+    return out
 
 
 # ---------------------------------------------------------------------------- emit
@@ -466,6 +557,18 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
             lines.append(f"  {d.ctype} {d.name};")
             declared.add(d.name)
     body_text = prog.text[kp.body[0]:kp.body[1]]
+    if kp.vec:
+        # vector loops: thread-strided headers, a block barrier after each
+        pieces, pos = [], kp.body[0]
+        for leaf, h in sorted(kp.vec, key=lambda x: x[0].span[0]):
+            hdr_end = h.body[0]
+            pieces.append(prog.text[pos:leaf.span[0]])
+            pieces.append(f"{{ for ({h.var} = ({h.lo}) + (long long)threadIdx.x * {h.step}; "
+                          f"{h.var} < ({h.hi}); {h.var} += (long long)blockDim.x * {h.step}) "
+                          f"{prog.text[hdr_end:leaf.span[1]]} __syncthreads(); }}")
+            pos = leaf.span[1]
+        pieces.append(prog.text[pos:kp.body[1]])
+        body_text = "".join(pieces)
     nl = len(kp.levels)
     total = " * ".join(f"hpg_n{i}" for i in range(nl))
     if kp.mode == "seq":
@@ -479,7 +582,9 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
         lines.append("}")
         return "\n".join(lines)
     lines.append(f"  const long long hpg_total = {total};")
-    if kp.mode == "block":
+    if kp.mode == "gang":
+        lines.append("  for (long long hpg_t = blockIdx.x; hpg_t < hpg_total; hpg_t += gridDim.x) {")
+    elif kp.mode == "block":
         lines.append("  if (blockIdx.x != 0) return;")
         lines.append("  for (long long hpg_t = threadIdx.x; hpg_t < hpg_total; hpg_t += blockDim.x) {")
     else:
@@ -520,8 +625,12 @@ def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
     total = " * ".join(f"hpg_n{i}" for i in range(len(kp.levels)))
     nred = len(kp.reductions) if kp.mode != "seq" else len(kp.privates)
     s.append(f"const long long hpg_total = {total};")
-    s.append(f"const int hpg_grid = R.grid_for(hpg_total, {'1' if kp.mode != 'grid' else '0'});")
-    s.append(f"const int hpg_block = {'1' if kp.mode == 'seq' else '256'};")
+    if kp.mode == "gang":
+        s.append("const int hpg_grid = R.gang_grid(hpg_total);")
+        s.append("const int hpg_block = 128;")
+    else:
+        s.append(f"const int hpg_grid = R.grid_for(hpg_total, {'1' if kp.mode != 'grid' else '0'});")
+        s.append(f"const int hpg_block = {'1' if kp.mode == 'seq' else '256'};")
     args = ["dev_struct(R)", "R.red_buffer(hpg_grid, " + str(max(nred, 1)) + ")"]
     for i in range(len(kp.levels)):
         args += [f"hpg_lo{i}", f"hpg_n{i}", f"hpg_st{i}"]
@@ -583,7 +692,7 @@ def generate(app: str, text: str, model, kinds: dict) -> str:
         kind = kinds.get(l.loop_id)
         if kind is None:
             continue
-        kp = plan_kernel(prog, l, kind, loops)
+        kp = plan_kernel(prog, l, kind, loops, kinds)
         if kp is None:
             notes[l.loop_id] = "loop header not recognised: host only"
             continue

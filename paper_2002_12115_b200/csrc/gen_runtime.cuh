@@ -289,6 +289,9 @@ class Runtime {
     const long long b = (total + 255) / 256;
     return (int)std::max<long long>(1, std::min<long long>(b, (long long)sms * 8));
   }
+  int gang_grid(long long total) const {
+    return (int)std::max<long long>(1, std::min<long long>(total, (long long)sms * 16));
+  }
   double* red_buffer(int grid, int nslots) {
     const size_t need = (size_t)grid * nslots;
     if (need > red_cap) {

@@ -333,36 +333,60 @@ class GenEvaluator:
             return MeasuredTime.timeout()
         return MeasuredTime.failed(res.diag.decode(errors="replace") or f"status {res.status}")
 
-    def verified_loops(self) -> list:
-        """Execution probe (the B200 analogue of the reference's compile probe,
-        classify.py:234-274): each classified loop alone on the GPU under its kind, its
-        stdout checked against the all-CPU program's with verify_results.  Loops the
-        static probe accepts but whose parallel execution changes the result (scalar- or
-        stage-carried chains, shared scratch) are dropped; ``probe_log`` keeps why."""
+    def verified_loops(self, trials: int = 2) -> list:
+        """Eligibility probe of the generated executor (the B200 analogue of the
+        reference's compile probe, classify.py:234-274), for every classified loop:
+
+        * static: a ``parallel loop`` / ``parallel loop vector`` with a loop-carried
+          scalar, or any loop whose iterations write the same array elements (an
+          output dependence, ``codegen.shared_writes``), is rejected -- the static
+          probe (classify.py:200-231) only looks at subscripts that use the index;
+        * execution: the loop alone on the GPU under its kind, ``trials`` runs, each
+          stdout checked against the all-CPU program's with verify_results.
+
+        ``probe_log`` keeps the reason per loop."""
+        from . import codegen
         from .tune import verify_results
+        prog = codegen.CProgram(self.spec.text())
         base = self.baseline_output()
         ok = []
         full = list(self.classified_ids)
+        full_planner = Planner(self.loops, self.refs, full)
         for lid in full:
-            g = tuple(int(l == lid) for l in full)
-            low = lower(g, full, self.kinds, self.loops, Planner(self.loops, self.refs, full).plan(g),
-                        self.lib, self.flags, self.timeout_s, self.nested_policy)
-            slot = self._free.get()
-            try:
-                ctx = self._context(slot)
-                res = ctx.run(low.schedule)
-                out = ctx.output()
-            finally:
-                self._free.put(slot)
-            if res.status != N.HP_OK:
-                self.probe_log[lid] = f"run failed: {res.diag.decode(errors='replace')}"
+            loop = self.loops.get(lid)
+            kind = self.kinds[lid].value
+            kp = codegen.plan_kernel(prog, loop, kind, self.loops)
+            if kp is not None and kp.carried and kind != "kernels":
+                self.probe_log[lid] = ("loop-carried scalar " + ", ".join(d.name for d in kp.carried)
+                                       + f" under {kind}")
                 continue
-            rep = verify_results(base, out)
-            if rep.passed:
+            shared = codegen.shared_writes(prog, loop)
+            if shared:
+                self.probe_log[lid] = "iterations write the same elements of " + ", ".join(shared)
+                continue
+            g = tuple(int(l == lid) for l in full)
+            low = lower(g, full, self.kinds, self.loops, full_planner.plan(g), self.lib,
+                        self.flags, self.timeout_s, self.nested_policy)
+            verdict = None
+            for _ in range(max(1, trials)):
+                slot = self._free.get()
+                try:
+                    ctx = self._context(slot)
+                    res = ctx.run(low.schedule)
+                    out = ctx.output()
+                finally:
+                    self._free.put(slot)
+                if res.status != N.HP_OK:
+                    verdict = f"run failed: {res.diag.decode(errors='replace')}"
+                    break
+                rep = verify_results(base, out)
+                if not rep.passed:
+                    verdict = "result differs: " + "; ".join(rep.detail[:1])
+                    break
+            if verdict is None:
                 ok.append(lid)
-                self.probe_log[lid] = f"verified ({self.lib.loop_notes[lid]}, {res.wall_s * 1e3:.1f} ms)"
-            else:
-                self.probe_log[lid] = "result differs: " + "; ".join(rep.detail[:1])
+                verdict = f"verified ({self.lib.loop_notes[lid]}, {res.wall_s * 1e3:.1f} ms)"
+            self.probe_log[lid] = verdict
         return ok
 
     def baseline_output(self) -> str:

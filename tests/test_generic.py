@@ -122,8 +122,11 @@ def test_ft_every_single_gene_runs(gpu):
 
 @pytest.mark.gpu
 def test_ft_verify_each_rejects_wrong_patterns(gpu):
+    # loops whose device result is deterministically wrong (carried scalar chains, FFT
+    # stage loops); the racy line-batch loops can come out right by timing and are
+    # rejected statically by the probe instead (test_ft_execution_probe)
     with generic.GenEvaluator("ft_s", devices=[0], verify_each=True) as ev:
-        for lid in FT_WRONG:
+        for lid in (6, 7, 12, 24, 36):
             m = ev.measure(_genome(ev, [lid]))
             assert m.failure and "differs" in m.failure, (lid, m)
         m = ev.measure(_genome(ev, FT_EXACT))

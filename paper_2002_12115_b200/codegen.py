@@ -338,6 +338,7 @@ class KernelPlan:
     mode: str             # "grid" | "gang" | "block" | "seq"
     note: str = ""
     vec: list = field(default_factory=list)   # [(LoopInfo, Header)] vector (thread) loops
+    write_refs: dict = field(default_factory=dict)   # array -> [[subscript tokens] per dim]
 
 
 def _vector_leaves(prog: CProgram, loop, loops, kinds) -> list:
@@ -403,12 +404,14 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
     arrays = sorted({n for n in names if n in prog.gmap and prog.gmap[n].is_array})
     writes = _writes(body_toks)
     arr_written = []
+    write_refs: dict = {}
     for k, t in enumerate(body_toks):
         if t.kind == "name" and t.text in arrays:
             # a[..][..] = / += / ++ : find the end of the subscript chain
             j = k + 1
+            subs = []
             while j < len(body_toks) and body_toks[j].text == "[":
-                depth, j = 0, j
+                depth, j0 = 0, j
                 while True:
                     if body_toks[j].text == "[":
                         depth += 1
@@ -417,9 +420,11 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
                         if depth == 0:
                             break
                     j += 1
+                subs.append(body_toks[j0 + 1:j])
                 j += 1
             if j < len(body_toks) and body_toks[j].text in ("=", "+=", "-=", "*=", "/=", "++", "--"):
                 arr_written.append(t.text)
+                write_refs.setdefault(t.text, []).append(subs)
     level_vars = {lv.var for lv in levels}
     params, privates, reds, carried = [], [], [], []
     seen = set()
@@ -458,7 +463,44 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
             mode = "gang"
             note = "vector " + ",".join(str(l.loop_id) for l, _ in vec)
     return KernelPlan(loop.loop_id, func, levels, body, arrays, sorted(set(arr_written)),
-                      params, privates, reds, carried, mode, note, vec)
+                      params, privates, reds, carried, mode, note, vec, write_refs)
+
+
+def write_boxes(prog: CProgram, kp: KernelPlan) -> dict:
+    """array -> (per-dim (lo, hi) C expressions evaluated on the host at launch, exact?)
+
+    A subscript is bounded exactly when it is a grid level's index (+- a constant), a
+    constant, or an expression of launch-invariant scalars (the kernel's read-only
+    arguments); anything else spans the whole dimension (inexact)."""
+    lv = {h.var: i for i, h in enumerate(kp.levels)}
+    fixed = {d.name for d in kp.params if d not in kp.carried}
+    out = {}
+    for name, refs in kp.write_refs.items():
+        dims = prog.gmap[name].dims
+        per_dim = [None] * len(dims)
+        exact = True
+        for subs in refs:
+            for d, sub in enumerate(subs):
+                txt = [t.text for t in sub]
+                rng = None
+                if len(txt) == 1 and txt[0] in lv:
+                    i = lv[txt[0]]
+                    rng = (f"hpg_lo{i}", f"hpg_lo{i} + (hpg_n{i} - 1) * hpg_st{i} + 1")
+                elif len(txt) == 3 and txt[0] in lv and txt[1] in "+-" and sub[2].kind == "num":
+                    i, c = lv[txt[0]], f"{txt[1]}{txt[2]}"
+                    rng = (f"hpg_lo{i} {c}", f"hpg_lo{i} + (hpg_n{i} - 1) * hpg_st{i} + 1 {c}")
+                elif all(t.kind == "num" or (t.kind == "name" and t.text in fixed) or
+                         (t.kind == "punct" and t.text in "+-*/%()") for t in sub) and sub:
+                    e = prog.text[sub[0].pos:sub[-1].pos + len(sub[-1].text)]
+                    rng = (f"(long long)({e})", f"(long long)({e}) + 1")
+                if rng is None:
+                    rng = ("0", str(dims[d]))
+                    exact = False
+                per_dim[d] = rng if per_dim[d] is None else \
+                    (f"std::min<long long>({per_dim[d][0]}, {rng[0]})",
+                     f"std::max<long long>({per_dim[d][1]}, {rng[1]})")
+        out[name] = (per_dim, exact)
+    return out
 
 
 def shared_writes(prog: CProgram, loop) -> list:
@@ -614,8 +656,11 @@ def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
     s = []
     s.append(f"static const int hpg_arr_{L}[] = {{{ids(kp.arrays)}}};")
     s.append(f"static const int hpg_wr_{L}[] = {{{ids(kp.arrays_written)}}};")
-    s.append(f"R.kernel_enter({L}, hpg_arr_{L}, {len(kp.arrays)}, hpg_wr_{L}, "
-             f"{len(kp.arrays_written)});")
+    boxes = write_boxes(prog, kp)
+    inexact = [n for n in kp.arrays_written if not boxes[n][1]]
+    s.append(f"static const int hpg_inexact_{L}[] = {{{ids(inexact)}}};")
+    s.append(f"R.kernel_enter({L}, hpg_arr_{L}, {len(kp.arrays)}, hpg_inexact_{L}, "
+             f"{len(inexact)});")
     for i, lv in enumerate(kp.levels):
         s.append(f"const long long hpg_lo{i} = (long long)({lv.lo});")
         s.append(f"const long long hpg_hi{i} = (long long)({lv.hi});")
@@ -638,6 +683,12 @@ def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
     s.append("if (hpg_total > 0) {")
     s.append(f"  k_{L}<<<hpg_grid, hpg_block, 0, R.stream>>>({', '.join(args)});")
     s.append(f"  R.launched({L});")
+    # the boxes this launch wrote (device-newer data a guarded copy-out moves back)
+    for name, (per_dim, exact) in write_boxes(prog, kp).items():
+        nd = len(per_dim)
+        s.append(f"  {{ const long long lo[{nd}] = {{{', '.join(p[0] for p in per_dim)}}}; "
+                 f"const long long hi[{nd}] = {{{', '.join(p[1] for p in per_dim)}}}; "
+                 f"R.dev_wrote(V_{name}, lo, hi, {nd}); }}")
     if kp.mode == "seq" and kp.privates:
         # one sequential device thread: its final scalars are the program's
         s.append(f"  double hpg_v[{len(kp.privates)}];")
@@ -747,6 +798,18 @@ def generate(app: str, text: str, model, kinds: dict) -> str:
         else:
             S.append(f"  {{\"{key}\", 0, 8}},")
     S.append("};")
+    for n, key in enumerate(var_keys):
+        d = prog.gmap.get(key)
+        dims = d.dims if d is not None and d.is_array else [1]
+        S.append(f"static const unsigned kDims_{n}[] = {{{', '.join(map(str, dims))}}};")
+    S.append("static const unsigned* const kDims[kVars] = {" +
+             ", ".join(f"kDims_{n}" for n in range(len(var_keys))) + "};")
+    S.append("static const int kNdims[kVars] = {" + ", ".join(
+        str(len(prog.gmap[k].dims)) if k in prog.gmap and prog.gmap[k].is_array else "1"
+        for k in var_keys) + "};")
+    S.append("static const unsigned long long kElems[kVars] = {" + ", ".join(
+        f"{prog.gmap[k].elems()}ull" if k in prog.gmap and prog.gmap[k].is_array else "1ull"
+        for k in var_keys) + "};")
     S.append("static const int kEligibleKind[kLoops] = {" + ", ".join(
         str({"kernels": 1, "parallel loop": 2, "parallel loop vector": 3}.get(kinds.get(l.loop_id), 0)
             if l.loop_id in launches else 0) for l in loops) + "};")
@@ -805,8 +868,8 @@ def generate(app: str, text: str, model, kinds: dict) -> str:
     S.append("  static constexpr int kVars = hpg_app_" + app + "::kVars;")
     S.append("  using Prog = hpg_app_" + app + "::Prog;")
     S.append("  static hpg::Tables tables() {")
-    S.append("    return hpg::Tables{kLoops, kVars, kVarDesc, kEligibleKind, kParent, kLoopWr, "
-             "kLoopWrN, kPreWr, kPreWrN};")
+    S.append("    return hpg::Tables{kLoops, kVars, kVarDesc, kDims, kNdims, kElems, kEligibleKind, "
+             "kParent, kLoopWr, kLoopWrN, kPreWr, kPreWrN};")
     S.append("  }")
     S.append("  static void bind(Prog* P, hpg::Runtime& R) { hpg_app_" + app + "::bind(P, R); }")
     S.append("};")

@@ -16,13 +16,15 @@
 //     events are counted (bytes, events) but move nothing;
 //   * a fresh run zeroes the program's statics (a new process) and treats device
 //     memory as undefined;
-//   * partial writes: a kernel that writes an array whose device copy is undefined
-//     or older than the host's (e.g. a plan `copyout` with no `copyin`, or host
-//     writes since the last copy) first gets the host copy (counted in n_guard_init
-//     and h2d bytes), so a later whole-array copy-out never carries undefined or
-//     stale device memory over newer host data -- the hazard of the reference's
-//     plans on real hardware.  The Himeno library guards the
-//     same hazard at box granularity without the extra copy.
+//   * device writes are tracked as boxes (each launch reports the box of every array
+//     it writes, computed on the host from the loop bounds -- codegen.write_boxes);
+//     a guarded copy-out moves only the boxes the device wrote since the array was
+//     last synchronised, so undefined or stale device memory never lands on newer
+//     host data (the hazard of the reference's plans on real hardware, SURVEY.md
+//     Appendix B.2; the Himeno library's coherence log does the same per box);
+//   * when a launch's write box is not exact (a subscript the generator cannot
+//     bound), an undefined or stale device copy is first refreshed from the host
+//     (counted in n_guard_init and h2d bytes), so the over-approximated box is safe.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -92,6 +94,9 @@ __device__ inline void block_reduce_store(double v, double* out, int slot, int n
 struct Tables {
   int nloops, nvars;
   const VarDesc* vars;
+  const unsigned* const* dims;   // per variable: extents (arrays)
+  const int* ndims;
+  const unsigned long long* elems;
   const int* elig_kind;
   const int* parent;
   const int* const* loop_wr;
@@ -123,6 +128,11 @@ class Runtime {
   double* h_red = nullptr;
   size_t red_cap = 0;
   std::vector<std::vector<int>> implicit_stack;
+  struct Box4 {
+    long long lo[4], hi[4];
+  };
+  std::vector<std::vector<Box4>> dirty;   // per array: device-written boxes since last sync
+  std::vector<char> dirty_full;
 
   ~Runtime() {
     if (d_red) cudaFree(d_red);
@@ -197,6 +207,53 @@ class Runtime {
     Rz->n_h2d++;
     if (implicit) Rz->n_implicit++;
     dev_ver[v] = host_ver[v];
+    dirty[v].clear();
+    dirty_full[v] = 0;
+  }
+  void dev_wrote(int v, const long long* lo, const long long* hi, int nd) {
+    const unsigned* dims = T.dims[v];
+    Box4 b;
+    bool full = true;
+    for (int d = 0; d < 4; ++d) {
+      const long long ext = d < nd ? (long long)dims[d] : 1;
+      b.lo[d] = d < nd ? std::max<long long>(0, lo[d]) : 0;
+      b.hi[d] = d < nd ? std::min<long long>(ext, hi[d]) : 1;
+      if (b.lo[d] >= b.hi[d]) return;   // empty launch
+      full = full && b.lo[d] == 0 && b.hi[d] == ext;
+    }
+    if (full || dirty[v].size() >= 64) {
+      dirty_full[v] = 1;
+      dirty[v].clear();
+    } else if (!dirty_full[v]) {
+      dirty[v].push_back(b);
+    }
+  }
+  // copy one box of array v device -> host (innermost three dims per memcpy3D)
+  void box_to_host(int v, const Box4& b, int nd) {
+    const unsigned* dims = T.dims[v];
+    const size_t esz = T.vars[v].bytes / T.elems[v];
+    long long ext[4], lo[4], hi[4];
+    for (int d = 0; d < 4; ++d) {   // right-align the dims into 4
+      const int s = d - (4 - nd);
+      ext[d] = s >= 0 ? dims[s] : 1;
+      lo[d] = s >= 0 ? b.lo[s] : 0;
+      hi[d] = s >= 0 ? b.hi[s] : 1;
+    }
+    const size_t row = (size_t)ext[3] * esz, plane = row * ext[2], vol = plane * ext[1];
+    for (long long i0 = lo[0]; i0 < hi[0]; ++i0) {
+      cudaMemcpy3DParms m = {};
+      char* hbase = (char*)host_ptr[v] + i0 * vol;
+      char* dbase = (char*)dev_ptr[v] + i0 * vol;
+      m.srcPtr = make_cudaPitchedPtr(dbase, row, (size_t)ext[3] * esz, (size_t)ext[2]);
+      m.dstPtr = make_cudaPitchedPtr(hbase, row, (size_t)ext[3] * esz, (size_t)ext[2]);
+      m.srcPos = make_cudaPos((size_t)lo[3] * esz, (size_t)lo[2], (size_t)lo[1]);
+      m.dstPos = m.srcPos;
+      m.extent = make_cudaExtent((size_t)(hi[3] - lo[3]) * esz, (size_t)(hi[2] - lo[2]),
+                                 (size_t)(hi[1] - lo[1]));
+      m.kind = cudaMemcpyDeviceToHost;
+      cuda(cudaMemcpy3DAsync(&m, stream), "d2h box");
+      Rz->d2h_bytes += m.extent.width * m.extent.height * m.extent.depth;
+    }
   }
   void d2h(int v, bool implicit) {
     const VarDesc& d = T.vars[v];
@@ -211,15 +268,27 @@ class Runtime {
       return;
     }
     const double t0 = now_s();
-    cuda(cudaMemcpyAsync(host_ptr[v], dev_ptr[v], d.bytes, cudaMemcpyDeviceToHost, stream), "d2h");
+    if (!guard || dirty_full[v]) {
+      cuda(cudaMemcpyAsync(host_ptr[v], dev_ptr[v], d.bytes, cudaMemcpyDeviceToHost, stream),
+           "d2h");
+      Rz->d2h_bytes += d.bytes;
+    } else {
+      // guarded: only what the device wrote since the last synchronisation
+      for (const Box4& b : dirty[v]) box_to_host(v, b, T.ndims[v]);
+    }
     cuda(cudaStreamSynchronize(stream), "d2h sync");
     Rz->xfer_s += now_s() - t0;
-    Rz->d2h_bytes += d.bytes;
+    dirty[v].clear();
+    dirty_full[v] = 0;
     Rz->n_d2h++;
     if (implicit) Rz->n_implicit++;
     host_ver[v] = dev_ver[v];
   }
-  void dealloc(int v) { dev_ver[v] = 0; }
+  void dealloc(int v) {
+    dev_ver[v] = 0;
+    dirty[v].clear();
+    dirty_full[v] = 0;
+  }
   void fire(const hpg_event* e) {
     const int v = e->var;
     switch (e->op) {
@@ -251,6 +320,7 @@ class Runtime {
   }
 
   // ---- kernels --------------------------------------------------------------
+  // wr: the arrays this launch writes with an inexact (over-approximated) box
   void kernel_enter(int L, const int* arrs, int n, const int* wr, int nw) {
     if (!has_dev) fail(ST_LAUNCH, "loop %d: no CUDA device in this context", L);
     implicit_stack.emplace_back();
@@ -365,6 +435,8 @@ class Runtime {
     dev_ver.assign(T.nvars, 0);
     refcount.assign(T.nvars, 0);
     declared.assign(T.nvars, 0);
+    dirty.assign(T.nvars, {});
+    dirty_full.assign(T.nvars, 0);
     clock = 1;
     guard = (s->flags & FLAG_GUARD) != 0;
     out.clear();

@@ -573,6 +573,8 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
     for d in kp.params:
         args.append(f"{d.ctype} hpg_p_{d.name}")
     lines.append(f"__global__ void __launch_bounds__(256) k_{kp.loop}({', '.join(args)}) {{")
+    lines.append('  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");')
+    lines.append('  asm volatile("griddepcontrol.wait;" ::: "memory");')
     for name in kp.arrays:
         lines.append(_array_ref(prog.gmap[name]))
     declared = set()
@@ -681,7 +683,7 @@ def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
         args += [f"hpg_lo{i}", f"hpg_n{i}", f"hpg_st{i}"]
     args += [d.name for d in kp.params]
     s.append("if (hpg_total > 0) {")
-    s.append(f"  k_{L}<<<hpg_grid, hpg_block, 0, R.stream>>>({', '.join(args)});")
+    s.append(f"  R.launch(k_{L}, hpg_grid, hpg_block, {', '.join(args)});")
     s.append(f"  R.launched({L});")
     # the boxes this launch wrote (device-newer data a guarded copy-out moves back)
     for name, (per_dim, exact) in write_boxes(prog, kp).items():

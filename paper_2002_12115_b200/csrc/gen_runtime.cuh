@@ -359,6 +359,22 @@ class Runtime {
     const long long b = (total + 255) / 256;
     return (int)std::max<long long>(1, std::min<long long>(b, (long long)sms * 8));
   }
+  // every generated kernel starts with griddepcontrol.launch_dependents + wait, so it
+  // can be launched with programmatic stream serialization: launch N+1 is scheduled
+  // while N runs, touches no data before N completed (loop-per-launch patterns)
+  template <typename... KArgs, typename... Args>
+  void launch(void (*kern)(KArgs...), int grid, int block, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
+  }
   int gang_grid(long long total) const {
     return (int)std::max<long long>(1, std::min<long long>(total, (long long)sms * 16));
   }

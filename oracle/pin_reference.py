@@ -157,7 +157,7 @@ def ft_genomes(n: int) -> list:
 def pin_ft():
     ev = ExternalEvaluator(CommandConfig("gcc -O2 -w {src} -o {bin} -lm", "{bin}", 600.0, 1),
                            build_variant=None)
-    for name in ("S", "W"):
+    for name in ("S", "W", "A"):
         c = ft.ft_class(name)
         fid, text = ft.source_file_id(c), ft.source_text(c)
         out = ev.run_for_output({fid: text})

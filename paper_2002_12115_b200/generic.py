@@ -52,10 +52,10 @@ def _himeno_spec():
 
 
 def app_specs() -> dict:
-    return {s.name: s for s in (_ft_spec("S"), _ft_spec("W"), _himeno_spec())}
+    return {s.name: s for s in (_ft_spec("S"), _ft_spec("W"), _ft_spec("A"), _himeno_spec())}
 
 
-APPS = ("ft_s", "ft_w", "himeno_xs")
+APPS = ("ft_s", "ft_w", "ft_a", "himeno_xs")
 
 
 class Event(C.Structure):

@@ -61,7 +61,7 @@ def analyze_ft(cls_name):
 
 
 def main_ft():
-    for name in ("S", "W"):
+    for name in ("S", "W", "A"):
         doc = analyze_ft(name)
         out = ROOT / "paper_2002_12115_b200" / "apps" / "model" / f"ft_{name.lower()}.json"
         out.write_text(json.dumps(doc, indent=1, sort_keys=True) + "\n")

@@ -2,7 +2,7 @@
 reference's own front-end and planner.
 
 * the reference's ExternalEvaluator stdout (gcc -O2, pragmas ignored; committed by
-  oracle/pin_reference.py) reproduces NPB FT's published class S / W checksums to NPB's
+  oracle/pin_reference.py) reproduces NPB FT's published class S / W / A checksums to NPB's
   1e-12 relative tolerance -- the restatement is the NPB algorithm;
 * the committed program model is the reference's analyze_project + StaticRuleProbe
   output (93 loops, 79 genes);
@@ -23,7 +23,7 @@ def _sig(e):
             e.close_file, list(e.close_span), list(e.present_sites), e.temp_region]
 
 
-@pytest.mark.parametrize("cls", ["S", "W"])
+@pytest.mark.parametrize("cls", ["S", "W", "A"])
 def test_reference_stdout_matches_npb_checksums(cls):
     out = (GOLDEN / f"ft_{cls.lower()}.stdout").read_text()
     assert ft.checksum_error(out, cls) <= ft.VERIFY_RTOL

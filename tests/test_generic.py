@@ -15,7 +15,8 @@ from conftest import GOLDEN
 from paper_2002_12115_b200 import codegen, generic
 from paper_2002_12115_b200.apps import ft, himeno
 
-GOLD = {"ft_s": "ft_s.stdout", "ft_w": "ft_w.stdout", "himeno_xs": "himeno_xs_n3.stdout"}
+GOLD = {"ft_s": "ft_s.stdout", "ft_w": "ft_w.stdout", "ft_a": "ft_a.stdout",
+        "himeno_xs": "himeno_xs_n3.stdout"}
 
 
 def test_codegen_parses_the_programs():
@@ -171,3 +172,43 @@ def test_ft_execution_probe(gpu):
         from paper_2002_12115_b200 import ga
         res = ga.run_ga(ga.GAConfig(population=6, generations=2, rng_seed=1), ev.gene_length, ev)
         assert res.best.time_s < 1000          # verified patterns only: a runnable best
+
+
+@pytest.mark.gpu
+def test_ft_class_a_exact_pattern_verifies_and_beats_cpu(gpu):
+    """Class A (256x256x128): the exact loops on the B200 reproduce NPB's checksums and run
+    faster than the all-CPU program."""
+    with generic.GenEvaluator("ft_a", devices=[0]) as ev:
+        prog = ft.program("A")
+        exact = [l for l in ev.eligible_ids if l in _ft_exact_ids(prog)]
+        g = _genome(ev, exact)
+        m = ev.measure(g)
+        assert m.seconds is not None, m
+        assert ft.checksum_error(ev.outputs[g], "A") <= 1e-9
+        cpu = ev.measure((0,) * ev.gene_length)
+        assert m.seconds < cpu.seconds, (m.seconds, cpu.seconds)
+
+
+def _ft_exact_ids(prog):
+    """Loops of an FT program whose device version is exact and which are not nested in
+    one another: collapsed kernels nests and gang loops with vector leaves, per the
+    structure of apps/ft.py (twiddle, seeds, plane fill, every copy / butterfly / evolve /
+    checksum loop)."""
+    from paper_2002_12115_b200 import codegen
+    p = codegen.CProgram(ft.source_text(prog.cls))
+    loops = prog.model.loops
+    out = []
+    for l in loops:
+        if l.loop_id not in prog.eligible:
+            continue
+        anc = loops.ancestors(l.loop_id)[1:]
+        if any(a in out for a in anc):
+            continue
+        kp = codegen.plan_kernel(p, l, prog.kinds[l.loop_id].value, loops, {k: v.value for k, v in prog.kinds.items()})
+        if kp is None or (kp.carried and kp.mode != "seq") or codegen.shared_writes(p, l):
+            continue
+        # FFT stage loops (l) carry data between iterations through the scratch rows
+        if l.index_var == "l" or l.index_var == "it":
+            continue
+        out.append(l.loop_id)
+    return out

@@ -228,4 +228,7 @@ def test_generated_himeno_random_patterns_match_hand_written(gpu):
             a = gen.run_for_output(g).split()
             b = hand.run_for_output(g).split()
             assert a[1:] == b[1:], (g, a, b)
-            assert abs(float(a[0]) - float(b[0])) <= 1e-5 * float(b[0]), (g, a[0], b[0])
+            # gosa: the generated executor's host stencil sums ss*ss in fp32 as the C
+            # program does, the hand-written library in fp64 (B.5): at
+            # XS the two differ by 0.04 %
+            assert abs(float(a[0]) - float(b[0])) <= 1e-3 * float(b[0]), (g, a[0], b[0])

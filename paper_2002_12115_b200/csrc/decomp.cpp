@@ -279,7 +279,9 @@ extern "C" int hp_dd_init(hp_ctx* c, int nranks, int rank, const unsigned char* 
   DD* d = new DD;
   d->nranks = nranks;
   d->rank = rank;
-  if (nranks > 1) {
+  // a communicator also for a single rank when an id is given (the NCCL transport
+  // then runs its all-reduce over one rank: how it is exercised on a 1-GPU box)
+  if (nranks > 1 || (id && n >= NCCL_UNIQUE_ID_BYTES)) {
     Nccl* l = nccl();
     if (!l) {
       delete d;
@@ -307,7 +309,7 @@ extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
     return HP_ERR_ARG;
   }
   DD* d = static_cast<DD*>(c->dd);
-  Nccl* l = d->nranks > 1 ? nccl() : nullptr;
+  Nccl* l = d->comm ? nccl() : nullptr;
   cudaSetDevice(c->device);
   const LaunchArgs a = ctx_args(c, 1);
   if (time_loop_begin(c, a) < 0) return cuda_fail(cudaGetLastError(), "begin");

@@ -161,6 +161,25 @@ def test_gpu_slab_single_rank_dd(gpu):
     s.close()
 
 
+@pytest.mark.gpu
+def test_gpu_slab_single_rank_over_nccl(gpu):
+    """hp_dd_* with a one-rank NCCL communicator: libnccl dlopen, ncclCommInitRank and the
+    gosa ncclAllReduce run on the device (the halo send/recv needs a second GPU)."""
+    sz = himeno.size("XS")
+    ref = oracle.run_program(sz.I, sz.J, sz.K, 3)
+    try:
+        uid = N.nccl_unique_id()
+    except Exception as exc:
+        pytest.skip(f"NCCL unavailable: {exc}")
+    s = dd.SlabJacobi("XS", 0, 1, 0)
+    s.ctx.dd_init(1, 0, uid)
+    s.ctx.init_device()
+    s.jacobi(3)
+    assert abs(s.gosa() - ref["gosa64"]) <= 1e-12 * ref["gosa64"]
+    assert np.array_equal(s.interior_p(), ref["fields"]["p"][1:sz.I - 2])
+    s.close()
+
+
 def _id_main(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)

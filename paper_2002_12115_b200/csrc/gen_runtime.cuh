@@ -133,6 +133,7 @@ class Runtime {
   };
   std::vector<std::vector<Box4>> dirty;   // per array: device-written boxes since last sync
   std::vector<char> dirty_full;
+  std::vector<char> dev_defined;          // device copy holds the whole array (a full h2d)
 
   ~Runtime() {
     if (d_red) cudaFree(d_red);
@@ -209,6 +210,7 @@ class Runtime {
     dev_ver[v] = host_ver[v];
     dirty[v].clear();
     dirty_full[v] = 0;
+    dev_defined[v] = 1;
   }
   void dev_wrote(int v, const long long* lo, const long long* hi, int nd) {
     const unsigned* dims = T.dims[v];
@@ -221,6 +223,7 @@ class Runtime {
       if (b.lo[d] >= b.hi[d]) return;   // empty launch
       full = full && b.lo[d] == 0 && b.hi[d] == ext;
     }
+    if (full) dev_defined[v] = 1;   // the device wrote every element
     if (full || dirty[v].size() >= 64) {
       dirty_full[v] = 1;
       dirty[v].clear();
@@ -288,6 +291,7 @@ class Runtime {
     dev_ver[v] = 0;
     dirty[v].clear();
     dirty_full[v] = 0;
+    dev_defined[v] = 0;
   }
   void fire(const hpg_event* e) {
     const int v = e->var;
@@ -332,13 +336,20 @@ class Runtime {
     }
     for (int x = 0; x < nw; ++x) {
       const int v = wr[x];
-      if (v >= 0 && T.vars[v].is_array && (dev_ver[v] == 0 || host_ver[v] > dev_ver[v])) {
-        const bool g = guard;
-        guard = false;
-        h2d(v, false);
-        guard = g;
-        Rz->n_guard_init++;
+      if (v < 0 || !T.vars[v].is_array || (dev_defined[v] && host_ver[v] <= dev_ver[v])) continue;
+      // an over-approximated write box needs a complete, current device copy: device
+      // writes not yet on the host go there first (exact boxes), then the full array
+      // goes to the device
+      if (!dirty[v].empty() && !dirty_full[v]) {
+        for (const Box4& b : dirty[v]) box_to_host(v, b, T.ndims[v]);
+        cuda(cudaStreamSynchronize(stream), "guard flush");
+        host_ver[v] = std::max(host_ver[v], dev_ver[v]);
       }
+      const bool g = guard;
+      guard = false;
+      h2d(v, false);
+      guard = g;
+      Rz->n_guard_init++;
     }
   }
   void kernel_exit(int L, const int* arrs, int n, const int* wr, int nw) {
@@ -453,6 +464,7 @@ class Runtime {
     declared.assign(T.nvars, 0);
     dirty.assign(T.nvars, {});
     dirty_full.assign(T.nvars, 0);
+    dev_defined.assign(T.nvars, 0);
     clock = 1;
     guard = (s->flags & FLAG_GUARD) != 0;
     out.clear();

@@ -708,7 +708,70 @@ def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
     return "\n".join(s)
 
 
-def transform_text(prog: CProgram, a: int, b: int, loops_by_start: dict, launches: dict) -> str:
+def host_write_boxes(prog: CProgram, loop, loops) -> list:
+    """Host code reporting the boxes loop `loop`'s own statements (not its nested
+    loops, which report their own) wrote, evaluated right after the loop ran on the
+    host: the loop's index spans its header range, scalars the body does not assign
+    are fixed, anything else spans the whole dimension."""
+    h = parse_header(prog, loop.span)
+    if h is None:
+        return []
+    kids = [loops.get(c).span for c in loops.children(loop.loop_id)]
+    toks = [t for t in prog.toks_in(*h.body) if not any(a <= t.pos < b for a, b in kids)]
+    assigned = set(_writes(prog.toks_in(*h.body)))
+    assigned.discard(h.var)
+    refs: dict = {}
+    for k, t in enumerate(toks):
+        if t.kind != "name" or t.text not in prog.gmap or not prog.gmap[t.text].is_array:
+            continue
+        j, subs = k + 1, []
+        while j < len(toks) and toks[j].text == "[":
+            depth, j0 = 0, j
+            while True:
+                if toks[j].text == "[":
+                    depth += 1
+                elif toks[j].text == "]":
+                    depth -= 1
+                    if depth == 0:
+                        break
+                j += 1
+            subs.append(toks[j0 + 1:j])
+            j += 1
+        if j < len(toks) and toks[j].text in ("=", "+=", "-=", "*=", "/=", "++", "--"):
+            refs.setdefault(t.text, []).append(subs)
+    out = []
+    hi_excl = f"(long long)({h.hi})"
+    for name, rlist in refs.items():
+        dims = prog.gmap[name].dims
+        per = [None] * len(dims)
+        for subs in rlist:
+            for d, sub in enumerate(subs):
+                txt = [x.text for x in sub]
+                rng = None
+                if txt == [h.var]:
+                    rng = (f"(long long)({h.lo})", hi_excl)
+                elif len(txt) == 3 and txt[0] == h.var and txt[1] in "+-" and sub[2].kind == "num":
+                    c = f"{txt[1]}{txt[2]}"
+                    rng = (f"(long long)({h.lo}) {c}", f"{hi_excl} {c}")
+                elif sub and all(x.kind == "num" or (x.kind == "name" and x.text not in assigned
+                                                      and x.text != h.var and x.text not in prog.gmap)
+                                 or (x.kind == "punct" and x.text in "+-*/%()") for x in sub):
+                    e = prog.text[sub[0].pos:sub[-1].pos + len(sub[-1].text)]
+                    rng = (f"(long long)({e})", f"(long long)({e}) + 1")
+                if rng is None:
+                    rng = ("0", str(dims[d]))
+                per[d] = rng if per[d] is None else \
+                    (f"std::min<long long>({per[d][0]}, {rng[0]})",
+                     f"std::max<long long>({per[d][1]}, {rng[1]})")
+        nd = len(dims)
+        out.append(f"{{ const long long lo[{nd}] = {{{', '.join(p[0] for p in per)}}}; "
+                   f"const long long hi[{nd}] = {{{', '.join(p[1] for p in per)}}}; "
+                   f"R.host_wrote(V_{name}, lo, hi, {nd}); }}")
+    return out
+
+
+def transform_text(prog: CProgram, a: int, b: int, loops_by_start: dict, launches: dict,
+                   loops=None) -> str:
     """Text [a, b) with every loop statement wrapped in its hooks (recursively)."""
     out, i = [], a
     starts = sorted(p for p in loops_by_start if a <= p < b)
@@ -718,14 +781,15 @@ def transform_text(prog: CProgram, a: int, b: int, loops_by_start: dict, launche
         s, e = loop.span
         out.append(prog.text[i:s])
         inner = transform_text(prog, s, e, {q: l for q, l in loops_by_start.items()
-                                            if s < q < e}, launches)
+                                            if s < q < e}, launches, loops)
         L = loop.loop_id
         dev = launches.get(L)
+        hw = " ".join(host_write_boxes(prog, loop, loops)) if loops is not None else ""
         if dev is not None:
-            out.append(f"{{ R.before({L}); if (R.dev({L})) {{\n{dev}\n}} else {inner} "
+            out.append(f"{{ R.before({L}); if (R.dev({L})) {{\n{dev}\n}} else {{ {inner} {hw} }} "
                        f"R.after({L}); }}")
         else:
-            out.append(f"{{ R.before({L}); R.host_only({L}); {inner} R.after({L}); }}")
+            out.append(f"{{ R.before({L}); R.host_only({L}); {inner} {hw} R.after({L}); }}")
         i = e
         starts = [q for q in starts if q >= e]
     out.append(prog.text[i:b])
@@ -856,7 +920,7 @@ def generate(app: str, text: str, model, kinds: dict) -> str:
     for f in prog.funcs:
         params = ", ".join(f"{d.ctype} {d.name}" for d in f.params)
         name = "main_" if f.name == "main" else f.name
-        body = transform_text(prog, f.body[0], f.body[1], loops_by_start, launches)
+        body = transform_text(prog, f.body[0], f.body[1], loops_by_start, launches, loops)
         S.append(f"  {f.ret} {name}({params}) {body}")
     S.append("};")
     S.append("static void bind(Prog* P, hpg::Runtime& R) {")

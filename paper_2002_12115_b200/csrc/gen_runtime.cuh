@@ -16,15 +16,18 @@
 //     events are counted (bytes, events) but move nothing;
 //   * a fresh run zeroes the program's statics (a new process) and treats device
 //     memory as undefined;
-//   * device writes are tracked as boxes (each launch reports the box of every array
-//     it writes, computed on the host from the loop bounds -- codegen.write_boxes);
-//     a guarded copy-out moves only the boxes the device wrote since the array was
-//     last synchronised, so undefined or stale device memory never lands on newer
-//     host data (the hazard of the reference's plans on real hardware, SURVEY.md
-//     Appendix B.2; the Himeno library's coherence log does the same per box);
-//   * when a launch's write box is not exact (a subscript the generator cannot
-//     bound), an undefined or stale device copy is first refreshed from the host
-//     (counted in n_guard_init and h2d bytes), so the over-approximated box is safe.
+//   * writes are tracked as boxes on both sides: each launch reports the box of every
+//     array it writes and each host-executed loop the box its own statements wrote,
+//     computed from the loop bounds (codegen.write_boxes / host_write_boxes); a
+//     guarded transfer moves exactly the source side's dirty boxes, or the whole array
+//     when the destination copy is undefined or the writes are unbounded -- so
+//     undefined or stale memory never lands on newer data (the hazard of the
+//     reference's plans on real hardware; the Himeno library's
+//     coherence log does the same per box) and a pattern pays only the bytes it changes;
+//   * a launch whose write box is not exact first brings an undefined or stale device
+//     copy up to date (n_guard_init), so the over-approximated box is safe;
+//   * small whole-array uploads go through a pinned staging ring without a host
+//     wait; large ones and box copies wait (the host may write the array next).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -133,9 +136,20 @@ class Runtime {
   };
   std::vector<std::vector<Box4>> dirty;   // per array: device-written boxes since last sync
   std::vector<char> dirty_full;
+  std::vector<std::vector<Box4>> hdirty;  // per array: host-written boxes since last sync
+  std::vector<char> hdirty_full;
   std::vector<char> dev_defined;          // device copy holds the whole array (a full h2d)
 
+  // pinned staging ring for small host -> device copies: the host copy is snapshotted
+  // into the ring and the transfer proceeds asynchronously, so the program keeps
+  // running (and may write the array again) while it is in flight
+  static constexpr size_t kStageSmall = 256 << 10;
+  static constexpr size_t kRingBytes = 64 << 20;
+  char* ring = nullptr;
+  size_t ring_off = 0;
+
   ~Runtime() {
+    if (ring) cudaFreeHost(ring);
     if (d_red) cudaFree(d_red);
     if (h_red) cudaFreeHost(h_red);
     for (void* p : dev_ptr)
@@ -168,8 +182,28 @@ class Runtime {
   void host_only(int L) {
     if (dev(L)) fail(ST_PATTERN, "loop %d has no device version", L);
   }
+  // host statements wrote these arrays somewhere (no box known): host-newer everywhere
   void host_writes(const int* v, int n) {
-    for (int x = 0; x < n; ++x) host_ver[v[x]] = ++clock;
+    for (int x = 0; x < n; ++x) {
+      if (v[x] < 0) continue;
+      host_ver[v[x]] = ++clock;
+      hdirty_full[v[x]] = 1;
+      hdirty[v[x]].clear();
+    }
+  }
+  // a host-executed loop reports the box its own statements wrote (codegen.write_boxes
+  // on the host version, evaluated after the loop)
+  void host_wrote(int v, const long long* lo, const long long* hi, int nd) {
+    host_ver[v] = ++clock;
+    if (hdirty_full[v]) return;
+    Box4 b;
+    if (!make_box(v, lo, hi, nd, b)) return;
+    if (is_full(v, b) || hdirty[v].size() >= 64) {
+      hdirty_full[v] = 1;
+      hdirty[v].clear();
+    } else if (!hdirty_full[v]) {
+      hdirty[v].push_back(b);
+    }
   }
   bool on_host(int L) const { return kind(L) == K_HOST; }
   void before(int L) {
@@ -182,12 +216,126 @@ class Runtime {
     for (const hpg_event* e : before_ev[L]) fire(e);
   }
   void after(int L) {
-    if (on_host(L)) host_writes(T.loop_wr[L], T.loop_wr_n[L]);
     for (const hpg_event* e : after_ev[L]) fire(e);
   }
 
   // ---- data manager ----------------------------------------------------------
+  // Each array has two dirty sets: boxes the host wrote since the device copy was last
+  // brought up to date, and boxes the device wrote since the host copy was.  A guarded
+  // transfer moves exactly the source's dirty boxes (both ways), or the whole array
+  // when the destination copy is undefined or the source's writes are unbounded; an
+  // unguarded one (HP flag off) is the literal whole-array copy.
   bool present(int v) const { return declared[v] || refcount[v] > 0; }
+  bool make_box(int v, const long long* lo, const long long* hi, int nd, Box4& b) const {
+    const unsigned* dims = T.dims[v];
+    for (int d = 0; d < 4; ++d) {
+      const long long ext = d < nd ? (long long)dims[d] : 1;
+      b.lo[d] = d < nd ? std::max<long long>(0, lo[d]) : 0;
+      b.hi[d] = d < nd ? std::min<long long>(ext, hi[d]) : 1;
+      if (b.lo[d] >= b.hi[d]) return false;   // empty
+    }
+    return true;
+  }
+  bool is_full(int v, const Box4& b) const {
+    for (int d = 0; d < T.ndims[v]; ++d)
+      if (b.lo[d] != 0 || b.hi[d] != (long long)T.dims[v][d]) return false;
+    return true;
+  }
+  size_t box_bytes(int v, const Box4& b) const {
+    size_t n = T.vars[v].bytes / T.elems[v];
+    for (int d = 0; d < T.ndims[v]; ++d) n *= (size_t)(b.hi[d] - b.lo[d]);
+    return n;
+  }
+  // boxes are worth it only when few and small: each strided copy costs a call
+  // (~10 us) where one contiguous whole-array copy streams at PCIe bandwidth
+  bool boxes_pay(int v, const std::vector<Box4>& bs) const {
+    if (bs.size() > 4) return false;
+    size_t sum = 0;
+    for (const Box4& b : bs) sum += box_bytes(v, b);
+    return sum * 4 <= T.vars[v].bytes;
+  }
+  // one box of array v between host and device (innermost three dims per memcpy3D;
+  // a box whose inner dimensions are full is one contiguous copy)
+  void copy_box(int v, const Box4& b, cudaMemcpyKind kind) {
+    {
+      const int nd = T.ndims[v];
+      int d0 = 0;   // first dim that is not a single index
+      while (d0 < nd && b.hi[d0] - b.lo[d0] == 1) ++d0;
+      bool contiguous = true;
+      for (int d = d0 + 1; d < nd; ++d)
+        contiguous = contiguous && b.lo[d] == 0 && b.hi[d] == (long long)T.dims[v][d];
+      if (contiguous) {
+        const size_t esz = T.vars[v].bytes / T.elems[v];
+        size_t off = 0;
+        for (int d = 0; d < nd; ++d) off = off * T.dims[v][d] + (size_t)b.lo[d];
+        const size_t bytes = box_bytes(v, b);
+        const bool up = kind == cudaMemcpyHostToDevice;
+        char* h = (char*)host_ptr[v] + off * esz;
+        char* dv = (char*)dev_ptr[v] + off * esz;
+        cuda(cudaMemcpyAsync(up ? dv : h, up ? h : dv, bytes, kind, stream),
+             up ? "h2d box" : "d2h box");
+        (up ? Rz->h2d_bytes : Rz->d2h_bytes) += bytes;
+        return;
+      }
+    }
+    const int nd = T.ndims[v];
+    const unsigned* dims = T.dims[v];
+    const size_t esz = T.vars[v].bytes / T.elems[v];
+    long long ext[4], lo[4], hi[4];
+    for (int d = 0; d < 4; ++d) {   // right-align the dims into 4
+      const int sd = d - (4 - nd);
+      ext[d] = sd >= 0 ? dims[sd] : 1;
+      lo[d] = sd >= 0 ? b.lo[sd] : 0;
+      hi[d] = sd >= 0 ? b.hi[sd] : 1;
+    }
+    const size_t row = (size_t)ext[3] * esz, vol = row * ext[2] * ext[1];
+    const bool up = kind == cudaMemcpyHostToDevice;
+    for (long long i0 = lo[0]; i0 < hi[0]; ++i0) {
+      cudaMemcpy3DParms m = {};
+      char* hbase = (char*)host_ptr[v] + i0 * vol;
+      char* dbase = (char*)dev_ptr[v] + i0 * vol;
+      const cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, row, row, (size_t)ext[2]);
+      const cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, row, row, (size_t)ext[2]);
+      m.srcPtr = up ? hp : dp;
+      m.dstPtr = up ? dp : hp;
+      m.srcPos = make_cudaPos((size_t)lo[3] * esz, (size_t)lo[2], (size_t)lo[1]);
+      m.dstPos = m.srcPos;
+      m.extent = make_cudaExtent((size_t)(hi[3] - lo[3]) * esz, (size_t)(hi[2] - lo[2]),
+                                 (size_t)(hi[1] - lo[1]));
+      m.kind = kind;
+      cuda(cudaMemcpy3DAsync(&m, stream), up ? "h2d box" : "d2h box");
+      const uint64_t bytes = (uint64_t)m.extent.width * m.extent.height * m.extent.depth;
+      (up ? Rz->h2d_bytes : Rz->d2h_bytes) += bytes;
+    }
+  }
+  void full_h2d(int v) {
+    const VarDesc& d = T.vars[v];
+    if (d.bytes <= kStageSmall) {
+      if (!ring && cudaMallocHost(&ring, kRingBytes) != cudaSuccess) {
+        ring = nullptr;
+        fail(ST_LAUNCH, "staging ring allocation failed");
+      }
+      if (ring_off + d.bytes > kRingBytes) {   // wrap: earlier copies out of the ring first
+        cuda(cudaStreamSynchronize(stream), "staging ring wrap");
+        ring_off = 0;
+      }
+      std::memcpy(ring + ring_off, host_ptr[v], d.bytes);
+      cuda(cudaMemcpyAsync(dev_ptr[v], ring + ring_off, d.bytes, cudaMemcpyHostToDevice, stream),
+           "h2d (staged)");
+      ring_off = (ring_off + d.bytes + 255) & ~(size_t)255;
+    } else {
+      cuda(cudaMemcpyAsync(dev_ptr[v], host_ptr[v], d.bytes, cudaMemcpyHostToDevice, stream),
+           "h2d");
+      cuda(cudaStreamSynchronize(stream), "h2d sync");
+    }
+    Rz->h2d_bytes += d.bytes;
+  }
+  void flush_dev_boxes(int v) {   // device-newer boxes -> host (before a whole-array h2d)
+    if (dirty[v].empty()) return;
+    for (const Box4& b : dirty[v]) copy_box(v, b, cudaMemcpyDeviceToHost);
+    cuda(cudaStreamSynchronize(stream), "flush device boxes");
+    dirty[v].clear();
+  }
   void h2d(int v, bool implicit) {
     const VarDesc& d = T.vars[v];
     if (!d.is_array) {   // host-authoritative scalar: counted only
@@ -196,66 +344,51 @@ class Runtime {
       return;
     }
     if (!has_dev) fail(ST_LAUNCH, "no device for update device(%s)", d.name);
-    if (guard && dev_ver[v] > host_ver[v]) {
-      Rz->n_skipped_stale++;
+    const double t0 = now_s();
+    if (!guard) {
+      full_h2d(v);
+      dirty[v].clear();
+      dirty_full[v] = 0;
+      dev_defined[v] = 1;
+    } else if (!dev_defined[v] || hdirty_full[v]) {
+      if (dirty_full[v] && dev_ver[v] > host_ver[v]) {   // device newer everywhere: stale update
+        Rz->n_skipped_stale++;
+        hdirty[v].clear();
+        hdirty_full[v] = 0;
+        return;
+      }
+      flush_dev_boxes(v);
+      full_h2d(v);
+      dev_defined[v] = 1;
+    } else if (!hdirty[v].empty()) {
+      if (boxes_pay(v, hdirty[v])) {
+        for (const Box4& b : hdirty[v]) copy_box(v, b, cudaMemcpyHostToDevice);
+        cuda(cudaStreamSynchronize(stream), "h2d boxes");
+      } else {
+        flush_dev_boxes(v);
+        full_h2d(v);
+      }
+    } else {
+      Rz->n_skipped_stale++;   // nothing the device does not already hold
       return;
     }
-    const double t0 = now_s();
-    cuda(cudaMemcpyAsync(dev_ptr[v], host_ptr[v], d.bytes, cudaMemcpyHostToDevice, stream), "h2d");
-    cuda(cudaStreamSynchronize(stream), "h2d sync");
+    hdirty[v].clear();
+    hdirty_full[v] = 0;
     Rz->xfer_s += now_s() - t0;
-    Rz->h2d_bytes += d.bytes;
     Rz->n_h2d++;
     if (implicit) Rz->n_implicit++;
-    dev_ver[v] = host_ver[v];
-    dirty[v].clear();
-    dirty_full[v] = 0;
-    dev_defined[v] = 1;
+    dev_ver[v] = std::max(dev_ver[v], host_ver[v]);
   }
   void dev_wrote(int v, const long long* lo, const long long* hi, int nd) {
-    const unsigned* dims = T.dims[v];
+    dev_ver[v] = ++clock;
     Box4 b;
-    bool full = true;
-    for (int d = 0; d < 4; ++d) {
-      const long long ext = d < nd ? (long long)dims[d] : 1;
-      b.lo[d] = d < nd ? std::max<long long>(0, lo[d]) : 0;
-      b.hi[d] = d < nd ? std::min<long long>(ext, hi[d]) : 1;
-      if (b.lo[d] >= b.hi[d]) return;   // empty launch
-      full = full && b.lo[d] == 0 && b.hi[d] == ext;
-    }
-    if (full) dev_defined[v] = 1;   // the device wrote every element
-    if (full || dirty[v].size() >= 64) {
+    if (!make_box(v, lo, hi, nd, b)) return;
+    if (is_full(v, b)) dev_defined[v] = 1;   // the device wrote every element
+    if (is_full(v, b) || dirty[v].size() >= 64) {
       dirty_full[v] = 1;
       dirty[v].clear();
     } else if (!dirty_full[v]) {
       dirty[v].push_back(b);
-    }
-  }
-  // copy one box of array v device -> host (innermost three dims per memcpy3D)
-  void box_to_host(int v, const Box4& b, int nd) {
-    const unsigned* dims = T.dims[v];
-    const size_t esz = T.vars[v].bytes / T.elems[v];
-    long long ext[4], lo[4], hi[4];
-    for (int d = 0; d < 4; ++d) {   // right-align the dims into 4
-      const int s = d - (4 - nd);
-      ext[d] = s >= 0 ? dims[s] : 1;
-      lo[d] = s >= 0 ? b.lo[s] : 0;
-      hi[d] = s >= 0 ? b.hi[s] : 1;
-    }
-    const size_t row = (size_t)ext[3] * esz, plane = row * ext[2], vol = plane * ext[1];
-    for (long long i0 = lo[0]; i0 < hi[0]; ++i0) {
-      cudaMemcpy3DParms m = {};
-      char* hbase = (char*)host_ptr[v] + i0 * vol;
-      char* dbase = (char*)dev_ptr[v] + i0 * vol;
-      m.srcPtr = make_cudaPitchedPtr(dbase, row, (size_t)ext[3] * esz, (size_t)ext[2]);
-      m.dstPtr = make_cudaPitchedPtr(hbase, row, (size_t)ext[3] * esz, (size_t)ext[2]);
-      m.srcPos = make_cudaPos((size_t)lo[3] * esz, (size_t)lo[2], (size_t)lo[1]);
-      m.dstPos = m.srcPos;
-      m.extent = make_cudaExtent((size_t)(hi[3] - lo[3]) * esz, (size_t)(hi[2] - lo[2]),
-                                 (size_t)(hi[1] - lo[1]));
-      m.kind = cudaMemcpyDeviceToHost;
-      cuda(cudaMemcpy3DAsync(&m, stream), "d2h box");
-      Rz->d2h_bytes += m.extent.width * m.extent.height * m.extent.depth;
     }
   }
   void d2h(int v, bool implicit) {
@@ -266,18 +399,28 @@ class Runtime {
       return;
     }
     if (!has_dev) fail(ST_LAUNCH, "no device for update self(%s)", d.name);
-    if (guard && host_ver[v] > dev_ver[v]) {
-      Rz->n_skipped_stale++;
-      return;
-    }
     const double t0 = now_s();
     if (!guard || dirty_full[v]) {
+      if (guard && hdirty_full[v] && host_ver[v] > dev_ver[v]) {   // host newer everywhere
+        Rz->n_skipped_stale++;
+        return;
+      }
       cuda(cudaMemcpyAsync(host_ptr[v], dev_ptr[v], d.bytes, cudaMemcpyDeviceToHost, stream),
            "d2h");
       Rz->d2h_bytes += d.bytes;
+    } else if (!dirty[v].empty()) {
+      if (boxes_pay(v, dirty[v]) || !dev_defined[v] || !hdirty[v].empty() || hdirty_full[v]) {
+        // (a whole-array copy is only safe when the device copy is complete and the
+        // host has no newer data)
+        for (const Box4& b : dirty[v]) copy_box(v, b, cudaMemcpyDeviceToHost);
+      } else {
+        cuda(cudaMemcpyAsync(host_ptr[v], dev_ptr[v], d.bytes, cudaMemcpyDeviceToHost, stream),
+             "d2h");
+        Rz->d2h_bytes += d.bytes;
+      }
     } else {
-      // guarded: only what the device wrote since the last synchronisation
-      for (const Box4& b : dirty[v]) box_to_host(v, b, T.ndims[v]);
+      Rz->n_skipped_stale++;   // the device wrote nothing since the last synchronisation
+      return;
     }
     cuda(cudaStreamSynchronize(stream), "d2h sync");
     Rz->xfer_s += now_s() - t0;
@@ -285,7 +428,7 @@ class Runtime {
     dirty_full[v] = 0;
     Rz->n_d2h++;
     if (implicit) Rz->n_implicit++;
-    host_ver[v] = dev_ver[v];
+    host_ver[v] = std::max(host_ver[v], dev_ver[v]);
   }
   void dealloc(int v) {
     dev_ver[v] = 0;
@@ -334,19 +477,14 @@ class Runtime {
       h2d(v, true);
       implicit_stack.back().push_back(v);
     }
+    // an over-approximated write box needs a complete, current device copy (else
+    // the later copy-out of the whole box would carry undefined or stale elements)
     for (int x = 0; x < nw; ++x) {
       const int v = wr[x];
-      if (v < 0 || !T.vars[v].is_array || (dev_defined[v] && host_ver[v] <= dev_ver[v])) continue;
-      // an over-approximated write box needs a complete, current device copy: device
-      // writes not yet on the host go there first (exact boxes), then the full array
-      // goes to the device
-      if (!dirty[v].empty() && !dirty_full[v]) {
-        for (const Box4& b : dirty[v]) box_to_host(v, b, T.ndims[v]);
-        cuda(cudaStreamSynchronize(stream), "guard flush");
-        host_ver[v] = std::max(host_ver[v], dev_ver[v]);
-      }
+      if (v < 0 || !T.vars[v].is_array) continue;
+      if (dev_defined[v] && !hdirty_full[v] && hdirty[v].empty()) continue;
       const bool g = guard;
-      guard = false;
+      guard = true;
       h2d(v, false);
       guard = g;
       Rz->n_guard_init++;
@@ -356,8 +494,8 @@ class Runtime {
     (void)L;
     (void)arrs;
     (void)n;
-    for (int x = 0; x < nw; ++x)
-      if (wr[x] >= 0) dev_ver[wr[x]] = ++clock;
+    (void)wr;
+    (void)nw;
     std::vector<int> imp = std::move(implicit_stack.back());
     implicit_stack.pop_back();
     for (int v : imp) {
@@ -464,6 +602,8 @@ class Runtime {
     declared.assign(T.nvars, 0);
     dirty.assign(T.nvars, {});
     dirty_full.assign(T.nvars, 0);
+    hdirty.assign(T.nvars, {});
+    hdirty_full.assign(T.nvars, 1);   // zeroed statics: defined on the host only
     dev_defined.assign(T.nvars, 0);
     clock = 1;
     guard = (s->flags & FLAG_GUARD) != 0;

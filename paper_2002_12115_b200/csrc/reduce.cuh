@@ -71,6 +71,7 @@ __device__ void gosa_commit_units(const GosaSink& g, uint32_t nunits, int reset)
   if (threadIdx.x == 0) {
     *g.slot = reset ? acc : (*g.slot + acc);
     *g.ticket = 0u;
+    *g.work = 0u;   // every unit was claimed: the queue is ready for the next launch
   }
 }
 

@@ -707,7 +707,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   if (units > g.capacity) return -1;   // one gosa partial per unit
   const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t) +
                       sizeof(UnitRing);
-  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
+  // the work-queue counter is zero: set at context creation, reset by the last CTA
   static bool attr_set[5] = {};   // per stage count: raise the dynamic smem limit once
   auto launch = [&](auto kern) {
     if (!attr_set[stages]) {
@@ -821,7 +821,7 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   if (grid > units) grid = units;
   if (units > g.capacity) return -1;   // one gosa partial per unit
   const size_t smem = T::smem_bytes();
-  if (cudaMemsetAsync(g.work, 0, sizeof(unsigned int), s) != cudaSuccess) return -1;
+  // the work-queue counter is zero: set at context creation, reset by the last CTA
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(k_stencil_tb2<LW, NW1, SC>,

@@ -232,3 +232,78 @@ def test_generated_himeno_random_patterns_match_hand_written(gpu):
             # program does, the hand-written library in fp64 (B.5): at
             # XS the two differ by 0.04 %
             assert abs(float(a[0]) - float(b[0])) <= 1e-3 * float(b[0]), (g, a[0], b[0])
+
+
+# ------------------------------------------------------------------ ABI (app_b200.h)
+
+def _declared_hpg():
+    import re
+    from conftest import ROOT
+    body = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "app_b200.h").read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(hpg_[a-z_0-9]+)\s*\(", body)))
+
+
+@pytest.mark.parametrize("app", generic.APPS)
+def test_generated_library_exports_every_declared_symbol(app):
+    lib = generic.load(app).lib
+    names = _declared_hpg()
+    assert "hpg_run" in names and "hpg_create" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) <= set(generic.SIGNATURES)
+
+
+def test_generated_struct_layouts_match_header(tmp_path):
+    import ctypes as C
+    import subprocess
+    from conftest import ROOT
+    structs = {"hpg_event": generic.Event, "hpg_schedule": generic.Schedule,
+               "hpg_result": generic.Result}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "app_b200.h"',
+             "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines) + "\n")
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(tmp_path / "p")],
+                   check=True)
+    got = {}
+    out = subprocess.run([str(tmp_path / "p")], capture_output=True, text=True, check=True).stdout
+    for line in out.splitlines():
+        cname, field, value = line.split()
+        got[(cname, field)] = int(value)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
+
+
+def _build_c_app(tmp_path):
+    import subprocess
+    from conftest import ROOT
+    lib_dir = ROOT / "paper_2002_12115_b200" / "_native"
+    exe = tmp_path / "c_app"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "c_app_example.c"), str(lib_dir / "libapp_ft_s.so"),
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_host_runs_generated_ft_on_cpu(tmp_path):
+    """A plain C program drives libapp_ft_s.so (host-only context): NPB checksums."""
+    import subprocess
+    out = subprocess.run([str(_build_c_app(tmp_path))], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout == (GOLDEN / "ft_s.stdout").read_text()
+
+
+@pytest.mark.gpu
+def test_c_host_runs_generated_ft_on_gpu(gpu, tmp_path):
+    import subprocess
+    out = subprocess.run([str(_build_c_app(tmp_path)), "gpu"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert ft.checksum_error(out.stdout, "S") <= 1e-9
+    assert "1 launches" in out.stderr or "launches" in out.stderr

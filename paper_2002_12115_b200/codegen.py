@@ -40,8 +40,6 @@ from typing import Optional
 TYPE_WORDS = ("void", "int", "long", "short", "char", "float", "double", "unsigned", "signed")
 KEYWORDS = set(TYPE_WORDS) | {"static", "const", "register", "for", "while", "if", "else",
                               "return", "break", "continue", "sizeof"}
-MATH = {"sqrt", "fabs", "sin", "cos", "tan", "exp", "log", "pow", "floor", "ceil", "fmin",
-        "fmax", "abs", "printf"}
 
 _TOKEN = re.compile(r"""
     (?P<ws>\s+|//[^\n]*|/\*.*?\*/)
@@ -293,7 +291,6 @@ def _writes(toks) -> dict:
 def _is_reduction(toks, name: str) -> bool:
     """Every occurrence of `name` is `name = name + e` / `name += e` with no other use."""
     occ = [k for k, t in enumerate(toks) if t.kind == "name" and t.text == name]
-    k = 0
     used = set()
     ok = False
     for i in occ:
@@ -319,7 +316,6 @@ def _is_reduction(toks, name: str) -> bool:
             ok = True
         else:
             return False
-        k += 1
     return ok
 
 
@@ -556,10 +552,6 @@ def shared_writes(prog: CProgram, loop) -> list:
 
 # ---------------------------------------------------------------------------- emit
 
-def _ctype(d: Decl) -> str:
-    return d.ctype
-
-
 def _array_ref(d: Decl) -> str:
     dims = "".join(f"[{n}]" for n in d.dims)
     return f"  {d.ctype} (&{d.name}){dims} = *reinterpret_cast<{d.ctype} (*){dims}>(D.{d.name});"
@@ -651,7 +643,7 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
     return "\n".join(lines)
 
 
-def emit_launch(prog: CProgram, kp: KernelPlan, host_loop_text: str) -> str:
+def emit_launch(prog: CProgram, kp: KernelPlan) -> str:
     """Host code replacing loop kp.loop when it runs on the device."""
     L = kp.loop
     ids = lambda names: ", ".join(f"V_{n}" for n in names) or "-1"   # noqa: E731
@@ -814,7 +806,7 @@ def generate(app: str, text: str, model, kinds: dict) -> str:
             notes[l.loop_id] = "loop header not recognised: host only"
             continue
         kernels.append(emit_kernel(prog, kp))
-        launches[l.loop_id] = emit_launch(prog, kp, "")
+        launches[l.loop_id] = emit_launch(prog, kp)
         kernel_modes[l.loop_id] = (kp.mode, len(kp.levels), kp.note)
     loops_by_start = {l.span[0]: l for l in loops}
 

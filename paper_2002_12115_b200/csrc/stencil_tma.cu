@@ -419,6 +419,116 @@ __device__ __forceinline__ void ss_quad(const float* ct, const Row& lm, const Ro
   for (int x = 0; x < 4; ++x) ss[x] = fmul(fsub(fmul(s0[x], el(a3, x)), el(m0.v, x)), el(bn, x));
 }
 
+// Paired fp32 (sm_100 FMUL2 / FADD2): two lanes of a quad per instruction, each
+// rounded separately -- bit-identical to the scalar ops.  ptxas contracts an
+// f32x2 multiply feeding an f32x2 add into FFMA2 even with --fmad=false (measured:
+// scratch probe, 25% of results differ), so products only ever feed scalar adds
+// here, and f32x2 adds only combine loaded values.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+
+// ss for a lane quad with paired products of the unshifted terms (a0, a1, b0, c0,
+// c1, a3, bnd); same per-element order of operations as ss_quad.
+template <int CS>
+__device__ __forceinline__ void ss_quad2(const float* ct, const Row& lm, const Row& l0,
+                                         const Row& lp, const Row& mm, const Row& m0,
+                                         const Row& mp, const Row& nm, const Row& n0,
+                                         const Row& np, float (&ss)[4]) {
+  auto Q = [&](int c) { return *reinterpret_cast<const float4*>(ct + c * CS); };
+  float s0[4];
+  auto acc2 = [&](float2 p01, float2 p23) {   // s0 += products (scalar adds)
+    s0[0] = fadd(s0[0], p01.x);
+    s0[1] = fadd(s0[1], p01.y);
+    s0[2] = fadd(s0[2], p23.x);
+    s0[3] = fadd(s0[3], p23.y);
+  };
+  {
+    const float4 q = Q(CA0);
+    const float2 p01 = mul2(lo2(q), lo2(n0.v)), p23 = mul2(hi2(q), hi2(n0.v));
+    s0[0] = p01.x; s0[1] = p01.y; s0[2] = p23.x; s0[3] = p23.y;
+  }
+  {
+    const float4 q = Q(CA1);
+    acc2(mul2(lo2(q), lo2(mp.v)), mul2(hi2(q), hi2(mp.v)));
+  }
+  {
+    const float4 q = Q(CA2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), kp1(m0, x)));
+  }
+  {
+    const float4 q = Q(CB0);
+    const float2 t01 = add2(sub2(sub2(lo2(np.v), lo2(nm.v)), lo2(lp.v)), lo2(lm.v));
+    const float2 t23 = add2(sub2(sub2(hi2(np.v), hi2(nm.v)), hi2(lp.v)), hi2(lm.v));
+    acc2(mul2(lo2(q), t01), mul2(hi2(q), t23));
+  }
+  {
+    const float4 q = Q(CB1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      s0[x] = fadd(s0[x], fmul(el(q, x), fadd(fsub(fsub(kp1(mp, x), kp1(mm, x)), km1(mp, x)),
+                                              km1(mm, x))));
+  }
+  {
+    const float4 q = Q(CB2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      s0[x] = fadd(s0[x], fmul(el(q, x), fadd(fsub(fsub(kp1(n0, x), kp1(l0, x)), km1(n0, x)),
+                                              km1(l0, x))));
+  }
+  {
+    const float4 q = Q(CC0);
+    acc2(mul2(lo2(q), lo2(l0.v)), mul2(hi2(q), hi2(l0.v)));
+  }
+  {
+    const float4 q = Q(CC1);
+    acc2(mul2(lo2(q), lo2(mm.v)), mul2(hi2(q), hi2(mm.v)));
+  }
+  {
+    const float4 q = Q(CC2);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], fmul(el(q, x), km1(m0, x)));
+  }
+  {
+    const float4 q = Q(CW1);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) s0[x] = fadd(s0[x], el(q, x));
+  }
+  const float4 a3 = Q(CA3), bn = Q(CBN);
+  // ss = (s0 * a3 - p) * bnd: product -> scalar sub -> paired product
+  const float2 u01 = mul2(make_float2(s0[0], s0[1]), lo2(a3));
+  const float2 u23 = mul2(make_float2(s0[2], s0[3]), hi2(a3));
+  const float2 d01 = make_float2(fsub(u01.x, m0.v.x), fsub(u01.y, m0.v.y));
+  const float2 d23 = make_float2(fsub(u23.x, m0.v.z), fsub(u23.y, m0.v.w));
+  const float2 r01 = mul2(d01, lo2(bn)), r23 = mul2(d23, hi2(bn));
+  ss[0] = r01.x; ss[1] = r01.y; ss[2] = r23.x; ss[3] = r23.y;
+}
+
 template <int LW, int NW1_, int SC_>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
@@ -538,7 +648,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         float v[4];
         if (plane_in && row_in) {
           float ss[4];
-          ss_quad<QK * R1>(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
+          ss_quad2<QK * R1>(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
 #pragma unroll
           for (int x = 0; x < 4; ++x) v[x] = in1[x] ? fadd(el(b0.v, x), fmul(omega, ss[x])) : el(b0.v, x);
         } else {
@@ -594,7 +704,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
           mbar_wait(&cfull[cslot], ((sc - 1) / SC) & 1);
           const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + (r2 + 1) * QK + hl * 4;
           float ss[4];
-          ss_quad<QK * R1>(ct, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
+          ss_quad2<QK * R1>(ct, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
           float w[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {

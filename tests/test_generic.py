@@ -307,3 +307,15 @@ def test_c_host_runs_generated_ft_on_gpu(gpu, tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert ft.checksum_error(out.stdout, "S") <= 1e-9
     assert "1 launches" in out.stderr or "launches" in out.stderr
+
+
+@pytest.mark.gpu
+def test_ft_screened_genes(gpu):
+    """genes="screened": verified loops that alone are no slower than the all-CPU program."""
+    with generic.GenEvaluator("ft_s", devices=[0], genes="screened",
+                              nested_policy="outermost", verify_each=True) as ev:
+        cpu = ev.probe_times["cpu"]
+        assert 0 < ev.gene_length < 64
+        for lid in ev.eligible_ids:
+            assert ev.probe_log[lid].startswith("verified")
+            assert ev.probe_times[lid] <= 1.05 * cpu

@@ -94,9 +94,13 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
                atol: float = DEFAULT_ATOL, rtol: float = DEFAULT_RTOL, echo=print) -> tuple:
     """Baseline, GA, verification and reports; returns (report document, verification ok)."""
     gene_len = evaluator.gene_length
+    if hasattr(evaluator, "size"):
+        what = (f"Himeno {evaluator.size.name} {evaluator.size.I}x{evaluator.size.J}x"
+                f"{evaluator.size.K}, nn={evaluator.nn}")
+    else:
+        what = f"generated executor {evaluator.spec.name}"
     echo(f"gene length {gene_len}; evaluator: B200 x {evaluator.max_concurrency} worker slot(s), "
-         f"Himeno {evaluator.size.name} {evaluator.size.I}x{evaluator.size.J}x{evaluator.size.K}, "
-         f"nn={evaluator.nn}")
+         f"{what}")
     t0 = time.perf_counter()
     baseline_s = measure_baseline(evaluator, gene_len)
     echo(f"baseline (all-CPU) time: {baseline_s:.6g} s")
@@ -158,7 +162,11 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
 
 
 def main(argv=None) -> int:
-    ap = argparse.ArgumentParser(description="GA offload search on B200s (Himeno)")
+    ap = argparse.ArgumentParser(description="GA offload search on B200s")
+    ap.add_argument("--app", default=None,
+                    help="a generated executor (generic.APPS, e.g. ft_s) instead of Himeno")
+    ap.add_argument("--genes", default="verified", choices=["all", "verified", "screened"],
+                    help="generated executors: the gene space (execution probe)")
     ap.add_argument("--size", default="M")
     ap.add_argument("--nn", type=int, default=3)
     ap.add_argument("--population", type=int, default=10)
@@ -180,6 +188,16 @@ def main(argv=None) -> int:
         workers = int(args.workers_per_device)
     cfg = ga.GAConfig(population=args.population, generations=args.generations,
                       rng_seed=args.seed)
+    if args.app:
+        from .generic import GenEvaluator
+        from . import native
+        devs = list(range(native.device_count())) if devices == "all" else devices
+        with GenEvaluator(args.app, devices=devs, workers_per_device=workers,
+                          transfer_mode=args.transfer_mode, nested_policy="outermost",
+                          verify_each=args.genes != "all",
+                          genes=None if args.genes == "all" else args.genes) as ev:
+            _report, ok = run_tuning(ev, cfg, args.out)
+        return 0 if ok else 3
     with B200Evaluator(args.size, nn=args.nn, devices=devices,
                        workers_per_device=workers,
                        transfer_mode=args.transfer_mode) as ev:

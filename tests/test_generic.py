@@ -319,3 +319,15 @@ def test_ft_screened_genes(gpu):
         for lid in ev.eligible_ids:
             assert ev.probe_log[lid].startswith("verified")
             assert ev.probe_times[lid] <= 1.05 * cpu
+
+
+@pytest.mark.gpu
+def test_tune_pipeline_on_ft(gpu, tmp_path):
+    """The tuning pipeline (baseline, GA, verify_results, reports) on a generated executor."""
+    from paper_2002_12115_b200 import tune
+    rc = tune.main(["--app", "ft_s", "--genes", "screened", "--population", "6",
+                    "--generations", "2", "--out", str(tmp_path)])
+    assert rc == 0
+    import json
+    rep = json.loads((tmp_path / "report.json").read_text())
+    assert rep["verification"]["status"] == "ran" and rep["verification"]["passed"]

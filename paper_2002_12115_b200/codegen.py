@@ -334,6 +334,7 @@ class KernelPlan:
     mode: str             # "grid" | "gang" | "block" | "seq"
     note: str = ""
     vec: list = field(default_factory=list)   # [(LoopInfo, Header)] vector (thread) loops
+    vsplit: bool = False  # vector loops may spread over several blocks per gang (no barriers)
     write_refs: dict = field(default_factory=dict)   # array -> [[subscript tokens] per dim]
 
 
@@ -453,13 +454,59 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
         body = h.body
         note = "loop-carried scalar " + ", ".join(d.name for d in carried)
     vec = []
+    vsplit = False
     if mode == "grid" and len(levels) == 1 and kinds is not None and not reds:
         vec = _vector_leaves(prog, loop, loops, kinds)
         if vec:
             mode = "gang"
             note = "vector " + ",".join(str(l.loop_id) for l, _ in vec)
+            # the vector loops need no block barrier when nothing the gang reads is
+            # written by a vector loop: then a gang's vector iterations may also be
+            # spread over several blocks (a 2-D grid), so a gang loop with few
+            # iterations (late FFT stages) still fills the GPU
+            leaf_written = set()
+            for leaf, _ in vec:
+                lt = prog.toks_in(*leaf.span)
+                for k, t in enumerate(lt):
+                    if t.kind == "name" and t.text in prog.gmap and prog.gmap[t.text].is_array:
+                        j = k + 1
+                        while j < len(lt) and lt[j].text == "[":
+                            depth = 0
+                            while True:
+                                if lt[j].text == "[":
+                                    depth += 1
+                                elif lt[j].text == "]":
+                                    depth -= 1
+                                    if depth == 0:
+                                        break
+                                j += 1
+                            j += 1
+                        if j < len(lt) and lt[j].text in ("=", "+=", "-=", "*=", "/=", "++", "--"):
+                            leaf_written.add(t.text)
+            read_anywhere = set()
+            for k, t in enumerate(body_toks):
+                if t.kind == "name" and t.text in leaf_written:
+                    # any occurrence that is not a pure store target counts as a read
+                    j = k + 1
+                    while j < len(body_toks) and body_toks[j].text == "[":
+                        depth = 0
+                        while True:
+                            if body_toks[j].text == "[":
+                                depth += 1
+                            elif body_toks[j].text == "]":
+                                depth -= 1
+                                if depth == 0:
+                                    break
+                            j += 1
+                        j += 1
+                    if not (j < len(body_toks) and body_toks[j].text == "="):
+                        read_anywhere.add(t.text)
+            vsplit = not read_anywhere
+            if vsplit:
+                note += " split"
     return KernelPlan(loop.loop_id, func, levels, body, arrays, sorted(set(arr_written)),
-                      params, privates, reds, carried, mode, note, vec, write_refs)
+                      params, privates, reds, carried, mode, note, vec=vec,
+                      write_refs=write_refs, vsplit=vsplit if mode == "gang" else False)
 
 
 def write_boxes(prog: CProgram, kp: KernelPlan) -> dict:
@@ -599,9 +646,15 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
         for leaf, h in sorted(kp.vec, key=lambda x: x[0].span[0]):
             hdr_end = h.body[0]
             pieces.append(prog.text[pos:leaf.span[0]])
-            pieces.append(f"{{ for ({h.var} = ({h.lo}) + (long long)threadIdx.x * {h.step}; "
-                          f"{h.var} < ({h.hi}); {h.var} += (long long)blockDim.x * {h.step}) "
-                          f"{prog.text[hdr_end:leaf.span[1]]} __syncthreads(); }}")
+            if kp.vsplit:
+                pieces.append(f"{{ for ({h.var} = ({h.lo}) + ((long long)blockIdx.y * blockDim.x + "
+                              f"threadIdx.x) * {h.step}; {h.var} < ({h.hi}); "
+                              f"{h.var} += (long long)gridDim.y * blockDim.x * {h.step}) "
+                              f"{prog.text[hdr_end:leaf.span[1]]} }}")
+            else:
+                pieces.append(f"{{ for ({h.var} = ({h.lo}) + (long long)threadIdx.x * {h.step}; "
+                              f"{h.var} < ({h.hi}); {h.var} += (long long)blockDim.x * {h.step}) "
+                              f"{prog.text[hdr_end:leaf.span[1]]} __syncthreads(); }}")
             pos = leaf.span[1]
         pieces.append(prog.text[pos:kp.body[1]])
         body_text = "".join(pieces)
@@ -667,6 +720,7 @@ def emit_launch(prog: CProgram, kp: KernelPlan) -> str:
     if kp.mode == "gang":
         s.append("const int hpg_grid = R.gang_grid(hpg_total);")
         s.append("const int hpg_block = 128;")
+        s.append(f"const int hpg_vsplit = {'R.vector_split(hpg_total)' if kp.vsplit else '1'};")
     else:
         s.append(f"const int hpg_grid = R.grid_for(hpg_total, {'1' if kp.mode != 'grid' else '0'});")
         s.append(f"const int hpg_block = {'1' if kp.mode == 'seq' else '256'};")
@@ -675,7 +729,10 @@ def emit_launch(prog: CProgram, kp: KernelPlan) -> str:
         args += [f"hpg_lo{i}", f"hpg_n{i}", f"hpg_st{i}"]
     args += [d.name for d in kp.params]
     s.append("if (hpg_total > 0) {")
-    s.append(f"  R.launch(k_{L}, hpg_grid, hpg_block, {', '.join(args)});")
+    if kp.mode == "gang":
+        s.append(f"  R.launch2(k_{L}, hpg_grid, hpg_vsplit, hpg_block, {', '.join(args)});")
+    else:
+        s.append(f"  R.launch(k_{L}, hpg_grid, hpg_block, {', '.join(args)});")
     s.append(f"  R.launched({L});")
     # the boxes this launch wrote (device-newer data a guarded copy-out moves back)
     for name, (per_dim, exact) in write_boxes(prog, kp).items():

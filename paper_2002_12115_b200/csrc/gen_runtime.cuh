@@ -524,6 +524,24 @@ class Runtime {
     cfg.numAttrs = 1;
     cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
   }
+  template <typename... KArgs, typename... Args>
+  void launch2(void (*kern)(KArgs...), int gx, int gy, int block, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(gx, gy);
+    cfg.blockDim = dim3(block);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
+  }
+  // blocks per gang when the vector loops need no barrier: fill about two waves
+  int vector_split(long long gangs) const {
+    const long long want = (2LL * sms + gangs - 1) / std::max<long long>(1, gangs);
+    return (int)std::max<long long>(1, std::min<long long>(want, 64));
+  }
   int gang_grid(long long total) const {
     return (int)std::max<long long>(1, std::min<long long>(total, (long long)sms * 16));
   }

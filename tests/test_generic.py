@@ -331,3 +331,18 @@ def test_tune_pipeline_on_ft(gpu, tmp_path):
     import json
     rep = json.loads((tmp_path / "report.json").read_text())
     assert rep["verification"]["status"] == "ran" and rep["verification"]["passed"]
+
+
+@pytest.mark.gpu
+def test_ft_random_verified_patterns_reproduce_npb(gpu):
+    """Random combinations of verified loops (nested genes under their outermost anchor):
+    every run reproduces NPB's checksums -- the data manager's hoisted transfers, dirty
+    boxes and staging are exact in combination, not only per loop."""
+    with generic.GenEvaluator("ft_s", devices=[0], genes="verified",
+                              nested_policy="outermost") as ev:
+        rng = random.Random(2002)
+        for _ in range(16):
+            g = tuple(rng.randint(0, 1) for _ in range(ev.gene_length))
+            m = ev.measure(g)
+            assert m.seconds is not None, m
+            assert ft.checksum_error(ev.outputs[g], "S") <= 1e-9, (g, ev.outputs[g])

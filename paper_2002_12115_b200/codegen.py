@@ -356,7 +356,21 @@ def _vector_leaves(prog: CProgram, loop, loops, kinds) -> list:
             kp = plan_kernel(prog, leaf, "parallel loop", loops)
             if kp is None or kp.carried or kp.reductions:
                 return
-            out.append((leaf, h))
+            # a parent whose body is exactly this loop, rectangular and free of
+            # carried scalars and output dependences, joins the vector region: its
+            # iterations and the leaf's are spread over the threads together
+            region, hs = leaf, [h]
+            par = loops.get(leaf.parent_loop) if leaf.parent_loop is not None else None
+            if par is not None and par.loop_id != loop.loop_id and par.shape == "tight_outer" \
+                    and loops.children(par.loop_id) == [lid]:
+                ph = parse_header(prog, par.span)
+                pkp = plan_kernel(prog, par, "parallel loop", loops) if ph else None
+                bound_names = set(_idents(tokenize(h.lo))) | set(_idents(tokenize(h.hi)))
+                if ph is not None and pkp is not None and not pkp.carried and \
+                        not pkp.reductions and not shared_writes(prog, par) and \
+                        ph.var not in bound_names:
+                    region, hs = par, [ph, h]
+            out.append((region, hs))
             return
         for c in kids:
             walk(c)
@@ -459,14 +473,17 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
         vec = _vector_leaves(prog, loop, loops, kinds)
         if vec:
             mode = "gang"
-            note = "vector " + ",".join(str(l.loop_id) for l, _ in vec)
+            note = "vector " + ",".join(
+                "x".join(str(loops.get(l.loop_id).loop_id) if len(hs) == 1 else
+                         f"{l.loop_id}" for _ in [0]) + ("+" if len(hs) > 1 else "")
+                for l, hs in vec)
             # the vector loops need no block barrier when nothing the gang reads is
             # written by a vector loop: then a gang's vector iterations may also be
             # spread over several blocks (a 2-D grid), so a gang loop with few
             # iterations (late FFT stages) still fills the GPU
             leaf_written = set()
             for leaf, _ in vec:
-                lt = prog.toks_in(*leaf.span)
+                lt = prog.toks_in(*leaf.span)   # (the vector region: leaf or its parent)
                 for k, t in enumerate(lt):
                     if t.kind == "name" and t.text in prog.gmap and prog.gmap[t.text].is_array:
                         j = k + 1
@@ -643,19 +660,30 @@ def emit_kernel(prog: CProgram, kp: KernelPlan) -> str:
     if kp.vec:
         # vector loops: thread-strided headers, a block barrier after each
         pieces, pos = [], kp.body[0]
-        for leaf, h in sorted(kp.vec, key=lambda x: x[0].span[0]):
-            hdr_end = h.body[0]
-            pieces.append(prog.text[pos:leaf.span[0]])
-            if kp.vsplit:
-                pieces.append(f"{{ for ({h.var} = ({h.lo}) + ((long long)blockIdx.y * blockDim.x + "
-                              f"threadIdx.x) * {h.step}; {h.var} < ({h.hi}); "
-                              f"{h.var} += (long long)gridDim.y * blockDim.x * {h.step}) "
-                              f"{prog.text[hdr_end:leaf.span[1]]} }}")
-            else:
-                pieces.append(f"{{ for ({h.var} = ({h.lo}) + (long long)threadIdx.x * {h.step}; "
-                              f"{h.var} < ({h.hi}); {h.var} += (long long)blockDim.x * {h.step}) "
-                              f"{prog.text[hdr_end:leaf.span[1]]} __syncthreads(); }}")
-            pos = leaf.span[1]
+        for region, hs in sorted(kp.vec, key=lambda x: x[0].span[0]):
+            inner = hs[-1]
+            pieces.append(prog.text[pos:region.span[0]])
+            body = prog.text[inner.body[0]:inner.body[1]]
+            start = "((long long)blockIdx.y * blockDim.x + threadIdx.x)" if kp.vsplit \
+                else "(long long)threadIdx.x"
+            stride = "(long long)gridDim.y * blockDim.x" if kp.vsplit else "(long long)blockDim.x"
+            ns = [f"((long long)({x.hi}) > (long long)({x.lo}) ? ((long long)({x.hi}) - "
+                  f"(long long)({x.lo}) + {x.step} - 1) / {x.step} : 0)" for x in hs]
+            decl = " ".join(f"const long long hv_n{i} = {n};" for i, n in enumerate(ns))
+            total = " * ".join(f"hv_n{i}" for i in range(len(hs)))
+            idx = []
+            for i in reversed(range(len(hs))):
+                x = hs[i]
+                if i:
+                    idx.append(f"{x.var} = (long long)({x.lo}) + (hv_q % hv_n{i}) * {x.step}; "
+                               f"hv_q /= hv_n{i};")
+                else:
+                    idx.append(f"{x.var} = (long long)({x.lo}) + hv_q * {x.step};")
+            barrier = "" if kp.vsplit else " __syncthreads();"
+            pieces.append(f"{{ {decl} for (long long hv_t = {start}; hv_t < {total}; "
+                          f"hv_t += {stride}) {{ long long hv_q = hv_t; {' '.join(idx)} "
+                          f"{body} }}{barrier} }}")
+            pos = region.span[1]
         pieces.append(prog.text[pos:kp.body[1]])
         body_text = "".join(pieces)
     nl = len(kp.levels)

@@ -473,10 +473,9 @@ def plan_kernel(prog: CProgram, loop, kind: str, loops, kinds=None) -> Optional[
         vec = _vector_leaves(prog, loop, loops, kinds)
         if vec:
             mode = "gang"
-            note = "vector " + ",".join(
-                "x".join(str(loops.get(l.loop_id).loop_id) if len(hs) == 1 else
-                         f"{l.loop_id}" for _ in [0]) + ("+" if len(hs) > 1 else "")
-                for l, hs in vec)
+            # vector regions: a leaf loop id, or "parent+" when its parent joined it
+            note = "vector " + ",".join(f"{r.loop_id}{'+' if len(hs) > 1 else ''}"
+                                        for r, hs in vec)
             # the vector loops need no block barrier when nothing the gang reads is
             # written by a vector loop: then a gang's vector iterations may also be
             # spread over several blocks (a 2-D grid), so a gang loop with few

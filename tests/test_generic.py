@@ -43,6 +43,15 @@ def test_kernel_plans_follow_the_directive_semantics():
     assert [d.name for d in kp.reductions] == ["cr", "ci"]
     kp = codegen.plan_kernel(p, loops.get(4), "parallel loop", loops)
     assert kp.mode == "grid" and "x" in [d.name for d in kp.privates] and not kp.carried
+    # the FFT butterfly loop i (parallel loop): one gang per i; its k x j nest is the
+    # vector region, spread over several blocks (nothing it writes is read in the gang)
+    kinds = {k: v.value for k, v in prog.kinds.items()}
+    kp = codegen.plan_kernel(p, loops.get(13), "parallel loop", loops, kinds)
+    assert kp.mode == "gang" and kp.vsplit
+    assert [(r.loop_id, [h.var for h in hs]) for r, hs in kp.vec] == [(14, ["k", "j"])]
+    # the line-batch loop a: its copy / stage loops need barriers between them
+    kp = codegen.plan_kernel(p, loops.get(9), "parallel loop", loops, kinds)
+    assert kp.mode == "gang" and not kp.vsplit and len(kp.vec) >= 3
 
 
 @pytest.mark.parametrize("app", generic.APPS)

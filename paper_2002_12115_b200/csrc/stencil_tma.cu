@@ -288,6 +288,9 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
 // Every product/sum rounds exactly like the single-step kernel: p2 is
 // bit-identical to two single steps; gosa (fp64) is that of the second step.
 constexpr int SP = 3, SQ = 4;  // p0 / p1 ring slots
+#ifndef HP_TB2_ROW_LDS
+#define HP_TB2_ROW_LDS 1
+#endif
 
 // LW lanes per row, NW1_ step-1 warps, SC_ coefficient ring slots
 template <int LW, int NW1_ = 8, int SC_ = 4>
@@ -331,10 +334,17 @@ __device__ __forceinline__ Row load_row0(const float* ptile, int row, int hl) {
   const float* base = ptile + row * (QK + 8);
   Row r;
   r.v = *reinterpret_cast<const float4*>(base + 4 + hl * 4);
+#if HP_TB2_ROW_LDS
+  // k-1 / k+4 straight from the tile row (the halo columns are in it): two loads,
+  // no shuffles or edge predicates
+  r.left = base[3 + hl * 4];
+  r.right = base[8 + hl * 4];
+#else
   r.left = __shfl_up_sync(0xffffffffu, r.v.w, 1, LW);
   r.right = __shfl_down_sync(0xffffffffu, r.v.x, 1, LW);
   if (hl == 0) r.left = base[3];
   if (hl == LW - 1) r.right = base[4 + QK];
+#endif
   return r;
 }
 // p1 tile row (QK floats): k+-1 by shuffles only (edge lanes never output)

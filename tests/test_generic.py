@@ -355,3 +355,26 @@ def test_ft_random_verified_patterns_reproduce_npb(gpu):
             m = ev.measure(g)
             assert m.seconds is not None, m
             assert ft.checksum_error(ev.outputs[g], "S") <= 1e-9, (g, ev.outputs[g])
+
+
+@pytest.mark.gpu
+def test_ft_class_w_exact_pattern(gpu):
+    with generic.GenEvaluator("ft_w", devices=[0]) as ev:
+        exact = _ft_exact_ids(ft.program("W"))
+        g = _genome(ev, [l for l in ev.eligible_ids if l in exact])
+        m = ev.measure(g)
+        assert m.seconds is not None, m
+        assert ft.checksum_error(ev.outputs[g], "W") <= 1e-9
+
+
+@pytest.mark.gpu
+def test_ft_per_loop_plan_is_wrong_for_evolve(gpu):
+    """The reference's raw per-loop directions give the evolve loop (49) u0 `copyin`
+    only, so its device update never returns: the batched plan verifies,
+    the per-loop one does not -- as an OpenACC build of those directives would."""
+    for mode, ok in (("batched", True), ("per-loop", False)):
+        with generic.GenEvaluator("ft_s", devices=[0], transfer_mode=mode) as ev:
+            g = _genome(ev, [49])
+            m = ev.measure(g)
+            assert m.seconds is not None, m
+            assert (ft.checksum_error(ev.outputs[g], "S") <= 1e-9) == ok, mode

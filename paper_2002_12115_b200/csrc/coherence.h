@@ -77,12 +77,11 @@ struct Coherence {
       nb = box_hull(log.back().box, nb);
       log.pop_back();
     }
-    std::vector<Span> kept;
-    kept.reserve(log.size() + 1);
-    for (const Span& e : log)
-      if (!box_contains(nb, e.box)) kept.push_back(e);
-    kept.push_back(Span{nb, owner});
-    log.swap(kept);
+    // in place (no allocation: row launches write once per launch)
+    log.erase(std::remove_if(log.begin(), log.end(),
+                             [&](const Span& e) { return box_contains(nb, e.box); }),
+              log.end());
+    log.push_back(Span{nb, owner});
   }
   // disjoint boxes whose latest writer is `owner`
   std::vector<Box> region(int owner) const {
@@ -99,9 +98,23 @@ struct Coherence {
     }
     return out;
   }
+  // does any point of b have `owner` as its latest writer?  Checks b's overlap with
+  // each `owner` entry minus the later entries, with reused scratch (called for every
+  // array at every launch)
   bool newer_in(int owner, const Box& b) const {
-    for (const Box& q : region(owner))
-      if (box_meets(q, b)) return true;
+    static thread_local std::vector<Box> pieces, next;
+    for (size_t n = 0; n < log.size(); ++n) {
+      if (log[n].owner != owner) continue;
+      const Box x = box_clip(log[n].box, b);
+      if (box_empty(x)) continue;
+      pieces.assign(1, x);
+      for (size_t m = n + 1; m < log.size() && !pieces.empty(); ++m) {
+        next.clear();
+        for (const Box& q : pieces) box_subtract(q, log[m].box, next);
+        pieces.swap(next);
+      }
+      if (!pieces.empty()) return true;
+    }
     return false;
   }
   // points whose latest writer is NOT `owner` (the region a guarded transfer

@@ -76,6 +76,32 @@ int main() {
     CHECK(vol(r.region(hp::OWN_DEV)) == in.count());
     CHECK(vol(r.region(hp::OWN_HOST)) == full.count() - in.count());
   }
+  // randomized: newer_in agrees with the explicit region (point test over the box)
+  {
+    unsigned seed = 12345;
+    auto rnd = [&](int n) { seed = seed * 1103515245u + 12345u; return (int)((seed >> 8) % (unsigned)n); };
+    const Box g{0, 6, 0, 5, 0, 7};
+    for (int trial = 0; trial < 300; ++trial) {
+      Coherence r;
+      r.reset(g);
+      const int nw = 1 + rnd(6);
+      for (int w = 0; w < nw; ++w) {
+        const int i0 = rnd(6), j0 = rnd(5), k0 = rnd(7);
+        const Box b{i0, i0 + 1 + rnd(6 - i0), j0, j0 + 1 + rnd(5 - j0), k0, k0 + 1 + rnd(7 - k0)};
+        r.write(b, rnd(3));
+        if (rnd(4) == 0) r.mark_synced(rnd(2));
+      }
+      for (int q = 0; q < 10; ++q) {
+        const int i0 = rnd(6), j0 = rnd(5), k0 = rnd(7);
+        const Box b{i0, i0 + 1 + rnd(6 - i0), j0, j0 + 1 + rnd(5 - j0), k0, k0 + 1 + rnd(7 - k0)};
+        for (int owner = 0; owner < 3; ++owner) {
+          bool want = false;
+          for (const Box& x : r.region(owner)) want = want || hp::box_meets(x, b);
+          CHECK(r.newer_in(owner, b) == want);
+        }
+      }
+    }
+  }
   std::printf("OK\n");
   return 0;
 }

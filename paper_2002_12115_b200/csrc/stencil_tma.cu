@@ -613,7 +613,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   } else if (warp < NW1) {
     // ------------------------------------- step-1 warps (tile row r = j0-1+r)
     const int r = warp * RPW + half;
-    uint32_t sp = 0, sc = 0, sq = 0;
+    uint32_t sc = 0, sq = 0;
+    int pslot = 0;          // p0 ring position, advanced incrementally (SP = 3 is not a
+    uint32_t pphase = 0;    // power of two: no division per plane)
     Unit s;
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
@@ -628,27 +630,33 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
 #pragma unroll
       for (int x = 0; x < 4; ++x) in1[x] = row_in && kq + x >= k_lo && kq + x < k_hi;
       Row am, a0, ap, bm, b0, bp;
+      auto next_p = [&]() {
+        if (++pslot == SP) {
+          pslot = 0;
+          pphase ^= 1u;
+        }
+      };
       for (int w = 0; w < 2; ++w) {
-        const int slot = sp % SP;
-        mbar_wait(&pfull[slot], (sp / SP) & 1);
+        const int slot = pslot;
+        mbar_wait(&pfull[slot], pphase);
         const float* pt = reinterpret_cast<const float*>(p0ring + slot * T::kP0Slot);
         const Row x0 = load_row0<LW>(pt, r, hl), x1 = load_row0<LW>(pt, r + 1, hl),
                   x2 = load_row0<LW>(pt, r + 2, hl);
         __syncwarp();
         if (lane == 0) mbar_arrive(&pempty[slot]);
         if (w == 0) { am = x0; a0 = x1; ap = x2; } else { bm = x0; b0 = x1; bp = x2; }
-        ++sp;
+        next_p();
       }
 #pragma unroll 1
       for (int m = ia - 1; m <= ib; ++m) {
-        const int pslot = sp % SP;
-        mbar_wait(&pfull[pslot], (sp / SP) & 1);
-        const float* pt = reinterpret_cast<const float*>(p0ring + pslot * T::kP0Slot);
+        const int cur = pslot;
+        mbar_wait(&pfull[cur], pphase);
+        const float* pt = reinterpret_cast<const float*>(p0ring + cur * T::kP0Slot);
         const Row cm = load_row0<LW>(pt, r, hl), c0 = load_row0<LW>(pt, r + 1, hl),
                   cp = load_row0<LW>(pt, r + 2, hl);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[pslot]);
-        ++sp;
+        if (lane == 0) mbar_arrive(&pempty[cur]);
+        next_p();
         const int cslot = sc % SC;
         mbar_wait(&cfull[cslot], (sc / SC) & 1);
         const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + r * QK + hl * 4;

@@ -18,13 +18,19 @@ time what an OpenACC compiler does for every directive the gene can select
   plan's events fire at the loop hooks (runtime: csrc/gen_runtime.cuh);
 * each eligible loop gets one sm_100a kernel ``k_L`` whose body is the loop's
   own source text over device arrays of the same names.  Directive kinds map
-  to launches as OpenACC defines them: ``kernels`` collapses the tight
+  to launches as OpenACC compilers map them: ``kernels`` collapses the tight
   rectangular nest below L into one grid (a loop with a loop-carried scalar
   runs as one sequential device thread, as an auto-parallelising compiler
-  leaves it), ``parallel loop`` spreads L's iterations over the grid,
-  ``parallel loop vector`` runs them in one thread block.  Scalars are
-  firstprivate kernel arguments; ``s = s + e`` / ``s += e`` accumulations are
-  reductions (fp64 block partials, folded in block order on the host).
+  leaves it); a loop that is not collapsed runs as gangs (one thread block per
+  iteration) whose innermost parallelisable loops -- with a tight independent
+  parent folded in -- are vector loops over the block's threads (a barrier after
+  each, or, when nothing they write is read in the gang, spread over several
+  blocks per gang); ``parallel loop vector`` runs in one thread block.  Scalars
+  are firstprivate kernel arguments; ``s = s + e`` / ``s += e`` accumulations
+  are reductions (fp64 block partials, folded in block order on the host);
+* every launch reports the boxes it writes and every host-executed loop the
+  boxes its own statements wrote (computed from the loop bounds), so the
+  runtime's transfers move only what changed.
 
 Parsing is limited to what the generator needs (declarations, function
 headers, ``for`` headers, identifier use); loop ids, spans, nesting and shapes

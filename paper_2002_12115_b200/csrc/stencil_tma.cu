@@ -100,19 +100,34 @@ struct Unit {           // one contiguous run of planes of one tile
   int kt, jt, ia, ib;
 };
 
-// Work units = (plane chunk, tile) in chunk-major order, handed out by the
-// device-wide queue (tma.cuh): CTAs that are resident together stream
-// neighbouring tiles over the same planes at the same time, so the halo rows a
-// tile shares with its neighbours are served from L2.
+// Work units, handed out by the device-wide queue (tma.cuh) in unit order.  The
+// first `full` units are whole tile columns (every plane of tiles 0..full-1);
+// the rest are (plane chunk, tile) pairs of the remaining tiles in chunk-major
+// order.  Either way the CTAs resident together stream neighbouring tiles over
+// the same planes at the same time, so the halo rows a tile shares with its
+// neighbours are served from L2, and a whole column pays no chunk boundary
+// (the two extra planes a unit loads and computes).
 struct Units {
-  int ni, ktiles, tiles, len;
+  int ni, ktiles, tiles, len, full;
   uint32_t count;
+  __device__ Units(int ni_, int ktiles_, int tiles_, int len_, int full_)
+      : ni(ni_), ktiles(ktiles_), tiles(tiles_), len(len_), full(full_),
+        count((uint32_t)(full_ + (tiles_ - full_) * ((ni_ + len_ - 1) / len_))) {}
   __device__ void decode(uint32_t u, Unit& s) const {
-    const int t = (int)(u % (uint32_t)tiles), c = (int)(u / (uint32_t)tiles);
+    int t, c;
+    if (u < (uint32_t)full) {
+      t = (int)u;
+      s.ia = 0;
+      s.ib = ni;
+    } else {
+      const uint32_t v = u - (uint32_t)full, rest = (uint32_t)(tiles - full);
+      t = full + (int)(v % rest);
+      c = (int)(v / rest);
+      s.ia = c * len;
+      s.ib = min(ni, s.ia + len);
+    }
     s.kt = t % ktiles;
     s.jt = t / ktiles;
-    s.ia = c * len;
-    s.ib = min(ni, s.ia + len);
   }
 };
 
@@ -131,8 +146,7 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
-  Units units{ni, ktiles, ktiles * jtiles, chunk,
-              (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
+  const Units units(ni, ktiles, ktiles * jtiles, chunk, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -543,7 +557,7 @@ template <int LW, int NW1_, int SC_>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
               int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
-              int g_lo, int g_hi, float omega, GosaSink g, int reset) {
+              int full, int g_lo, int g_hi, float omega, GosaSink g, int reset) {
   using T = Tb2<LW, NW1_, SC_>;
   constexpr int RPW = T::RPW, NW1 = T::NW1, NW2 = T::NW2, R1 = T::R1, TJ2 = T::TJ2,
                 QK = T::QK, TK2 = T::TK2, SC = T::SC;
@@ -565,8 +579,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  Units units{ni, ktiles, ktiles * jtiles, chunk,
-              (uint32_t)(ktiles * jtiles * ((ni + chunk - 1) / chunk))};
+  const Units units(ni, ktiles, ktiles * jtiles, chunk, full);
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
     for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], NW1 + NW2); }
@@ -784,20 +797,25 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   TmaState* t = new TmaState;
   int pc[4];
   promo_codes(pc);
+  // row extent the maps expose: K (columns past it are zero-filled by TMA, never
+  // read) or the padded pitch P
+  int dk = F.K;
+  if (const char* e = getenv("HIMENO_TMA_DIMK")) dk = atoi(e) ? F.K : F.P;
   bool ok = true;
   for (int m = 0; m < NCOEF; ++m) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ, pc[0]);
+    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ, pc[0], dk);
   }
-  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1]);
-  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1]);
+  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1], dk);
+  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1], dk);
   auto encode_tb2 = [&](Tb2Maps& maps, CUtensorMap& scr, int qk, int r1) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    for (int m = 0; m < NCOEF; ++m) ok = ok && encode(&maps.coef[m], F, F.f[fields[m]], qk, r1, pc[2]);
-    ok = ok && encode(&maps.pin, F, F.f[HP_F_P], qk + 8, r1 + 2, pc[3]);
-    ok = ok && encode(&scr, F, scratch, qk + 8, r1 + 2, pc[3]);
+    for (int m = 0; m < NCOEF; ++m)
+      ok = ok && encode(&maps.coef[m], F, F.f[fields[m]], qk, r1, pc[2], dk);
+    ok = ok && encode(&maps.pin, F, F.f[HP_F_P], qk + 8, r1 + 2, pc[3], dk);
+    ok = ok && encode(&scr, F, scratch, qk + 8, r1 + 2, pc[3], dk);
   };
   encode_tb2(t->tb2[0], t->tb2_scratch[0], Tb2<32, 8, 4>::QK, Tb2<32, 8, 4>::R1);
   encode_tb2(t->tb2[1], t->tb2_scratch[1], Tb2<16, 8, 4>::QK, Tb2<16, 8, 4>::R1);
@@ -874,35 +892,41 @@ static long long tb2_tiles(int nj, int k_hi) {
   return (long long)((k_hi + T::TK2 - 1) / T::TK2) * ((nj + T::TJ2 - 1) / T::TJ2);
 }
 
-// Makespan of one pass: the device-wide queue hands the chunk-major units to
-// the first free CTA (list scheduling); a unit of n planes takes n + 2 plane
-// steps (two warm-up planes) at the shape's per-step cost (microseconds per
-// plane step of one CTA, measured on the L grid: profiles/r01_tb2_shapes.txt).
-static double tb2_makespan(long long tiles, int ni, int chunk, int sms, double cost) {
+// Makespan of one pass: the device-wide queue hands the units (`full` whole
+// columns, then the chunk-major units of the other tiles) to the first free CTA
+// (list scheduling); a unit of n planes takes n + 2 plane steps (two warm-up
+// planes) at the shape's per-step cost (microseconds per plane step of one CTA,
+// measured on the L grid: profiles/r01_tb2_shapes.txt).
+static double tb2_makespan(long long tiles, int ni, int chunk, long long full, int sms,
+                           double cost) {
   std::priority_queue<double, std::vector<double>, std::greater<double>> q;
-  const long long total = tiles * ((ni + chunk - 1) / chunk);
+  const long long total = full + (tiles - full) * ((ni + chunk - 1) / chunk);
   for (long long c = 0; c < std::min<long long>(sms, total); ++c) q.push(0.0);
   double end = 0.0;
+  auto run = [&](double d) {
+    const double f = q.top() + d;
+    q.pop();
+    q.push(f);
+    end = std::max(end, f);
+  };
+  for (long long t = 0; t < full; ++t) run((double)(ni + 2) * cost);
   for (int c0 = 0; c0 < ni; c0 += chunk) {
     const double d = (double)(std::min(chunk, ni - c0) + 2) * cost;
-    for (long long t = 0; t < tiles; ++t) {
-      const double f = q.top() + d;
-      q.pop();
-      q.push(f);
-      end = std::max(end, f);
-    }
+    for (long long t = full; t < tiles; ++t) run(d);
   }
   return end;
 }
 
-// (shape, planes per unit) with the least predicted makespan, cached per pass
-// geometry; HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK pin either for sweeps.
+// (shape, planes per unit, whole columns) with the least predicted makespan,
+// cached per pass geometry; HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK pin the first
+// two for sweeps, HIMENO_TB2_FULL=0 disables whole-column units.
 struct Tb2Choice {
-  int shape, chunk;
+  int shape, chunk, full;
 };
 static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
   static const double cost[kTb2Shapes] = {1.03, 1.04, 0.91, 0.885};
   const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_TB2_CHUNK");
+  const bool use_full = env_int("HIMENO_TB2_FULL") != 0;
   const bool pinned = pin_shape >= 0 || pin_chunk > 0;
   static std::mutex mu;
   static std::map<std::array<int, 4>, Tb2Choice> cache;
@@ -912,7 +936,7 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  Tb2Choice best{1, 64};
+  Tb2Choice best{1, 64, 0};
   double best_t = 1e300;
   for (int v = 0; v < kTb2Shapes; ++v) {
     if (pin_shape >= 0 && pin_shape < kTb2Shapes && v != pin_shape) continue;
@@ -923,11 +947,15 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
       case 2: tiles = tb2_tiles<16, 6, 5>(nj, k_hi); break;
       default: tiles = tb2_tiles<16, 5, 6>(nj, k_hi); break;
     }
-    for (int chunk = 16; chunk <= 128; chunk += 8) {
-      const int ch = pin_chunk > 0 ? pin_chunk : chunk;
-      const double t = tb2_makespan(tiles, ni, ch, sms, cost[v]);
-      if (t < best_t) { best_t = t; best = {v, ch}; }
-      if (pin_chunk > 0) break;
+    // whole columns: none, or every full wave of tiles (the remainder is chunked)
+    const long long fulls[2] = {0, use_full ? tiles / sms * sms : 0};
+    for (long long full : fulls) {
+      for (int chunk = 16; chunk <= 128; chunk += 8) {
+        const int ch = pin_chunk > 0 ? pin_chunk : chunk;
+        const double t = tb2_makespan(tiles, ni, ch, full, sms, cost[v]);
+        if (t < best_t) { best_t = t; best = {v, ch, (int)full}; }
+        if (pin_chunk > 0) break;
+      }
     }
   }
   if (!pinned) {
@@ -940,11 +968,13 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
 template <int LW, int NW1, int SC>
 static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int i_lo, int i_hi,
                       int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
-                      const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+                      int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
   using T = Tb2<LW, NW1, SC>;
   const int ktiles = (k_hi + T::TK2 - 1) / T::TK2;
   const int jtiles = (j_hi - j_lo + T::TJ2 - 1) / T::TJ2;
-  const long long units = (long long)ktiles * jtiles * ((i_hi - i_lo + chunk - 1) / chunk);
+  const long long tiles = (long long)ktiles * jtiles;
+  if (full < 0 || full > tiles) full = 0;
+  const long long units = full + (tiles - full) * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
   if (grid > units) grid = units;
   if (units > g.capacity) return -1;   // one gosa partial per unit
@@ -958,8 +988,8 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
     attr = true;
   }
   k_stencil_tb2<LW, NW1, SC><<<(int)grid, T::kThreads, smem, s>>>(
-      maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, g_lo, g_hi, a.omega, g,
-      a.gosa_reset);
+      maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, full, g_lo, g_hi,
+      a.omega, g, a.gosa_reset);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -983,7 +1013,7 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (p_in == t->scratch) maps.pin = t->tb2_scratch[v];
 #define HP_TB2(LW, NW1, SC) \
   launch_tb2<LW, NW1, SC>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, c.chunk, \
-                          a, g, s, sms)
+                          c.full, a, g, s, sms)
   switch (v) {
     case 1: return HP_TB2(16, 8, 4);
     case 2: return HP_TB2(16, 6, 5);

@@ -919,15 +919,16 @@ static double tb2_makespan(long long tiles, int ni, int chunk, long long full, i
 
 // (shape, planes per unit, whole columns) with the least predicted makespan,
 // cached per pass geometry; HIMENO_TB2_SHAPE / HIMENO_TB2_CHUNK pin the first
-// two for sweeps, HIMENO_TB2_FULL=0 disables whole-column units.
+// two for sweeps; HIMENO_TB2_FULL=0 disables whole-column units, =1 leaves them
+// to the model, =n >= 2 pins n of them (tests).
 struct Tb2Choice {
   int shape, chunk, full;
 };
 static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
   static const double cost[kTb2Shapes] = {1.03, 1.04, 0.91, 0.885};
   const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_TB2_CHUNK");
-  const bool use_full = env_int("HIMENO_TB2_FULL") != 0;
-  const bool pinned = pin_shape >= 0 || pin_chunk > 0;
+  const int pin_full = env_int("HIMENO_TB2_FULL");
+  const bool pinned = pin_shape >= 0 || pin_chunk > 0 || pin_full >= 0;
   static std::mutex mu;
   static std::map<std::array<int, 4>, Tb2Choice> cache;
   const std::array<int, 4> key{ni, nj, k_hi, sms};
@@ -948,7 +949,8 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
       default: tiles = tb2_tiles<16, 5, 6>(nj, k_hi); break;
     }
     // whole columns: none, or every full wave of tiles (the remainder is chunked)
-    const long long fulls[2] = {0, use_full ? tiles / sms * sms : 0};
+    long long fulls[2] = {0, pin_full != 0 ? tiles / sms * sms : 0};
+    if (pin_full >= 2) fulls[0] = fulls[1] = std::min<long long>(pin_full, tiles);
     for (long long full : fulls) {
       for (int chunk = 16; chunk <= 128; chunk += 8) {
         const int ch = pin_chunk > 0 ? pin_chunk : chunk;

@@ -261,6 +261,32 @@ def test_two_step_shapes_bit_exact(gpu, monkeypatch, shape, chunk):
     assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
 
 
+@pytest.mark.parametrize("full", [0, 2, 5, 9])
+def test_two_step_whole_columns_bit_exact(gpu, monkeypatch, full):
+    """Whole tile columns ahead of the chunked tail (HIMENO_TB2_FULL pins how many; the
+    grid has 3 x 3 tiles of shape (16,8,4), so 9 = every tile a whole column) give the
+    same field, bit for bit, as the oracle."""
+    sz = himeno.custom_size(75, 45, 141)
+    nn = 4
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    monkeypatch.setenv("HIMENO_TB2_SHAPE", "1")
+    monkeypatch.setenv("HIMENO_TB2_CHUNK", "16")
+    monkeypatch.setenv("HIMENO_TB2_FULL", str(full))
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(1)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+            kt = ctx.time_jacobi(nn, 1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    assert kt.stencil_iters == 2.0
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+
+
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("name,nn", [("XS", 1), ("XS", 4), ("XS", 5), ("M", 2), ("M", 3),
                                       ("custom", 4), ("ragged", 3)])

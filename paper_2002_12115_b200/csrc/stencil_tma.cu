@@ -590,6 +590,11 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // launched with programmatic stream serialization: the next pass may be
+  // scheduled as SMs free up, but nothing global (queue counter, fields, gosa)
+  // is touched before the previous grid has completed and flushed
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   double acc = 0.0;
   if (warp == NW1 + NW2) {
     // ------------------------------------------------------------- producer
@@ -989,10 +994,21 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
       return -1;
     attr = true;
   }
-  k_stencil_tb2<LW, NW1, SC><<<(int)grid, T::kThreads, smem, s>>>(
-      maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, full, g_lo, g_hi,
-      a.omega, g, a.gosa_reset);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  static const bool pdl = env_int("HIMENO_TB2_PDL") != 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(T::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC>, maps, F, p_out, i_lo,
+                                           i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, full, g_lo,
+                                           g_hi, a.omega, g, a.gosa_reset);
+  return e == cudaSuccess ? 1 : -1;
 }
 
 // Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not

@@ -556,8 +556,8 @@ __device__ __forceinline__ void ss_quad2(const float* ct, const Row& lm, const R
 template <int LW, int NW1_, int SC_>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
-              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int chunk,
-              int full, int g_lo, int g_hi, float omega, GosaSink g, int reset) {
+              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int k_org, int ktiles,
+              int chunk, int full, int g_lo, int g_hi, float omega, GosaSink g, int reset) {
   using T = Tb2<LW, NW1_, SC_>;
   constexpr int RPW = T::RPW, NW1 = T::NW1, NW2 = T::NW2, R1 = T::R1, TJ2 = T::TJ2,
                 QK = T::QK, TK2 = T::TK2, SC = T::SC;
@@ -606,7 +606,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         if (u == kNoUnit) break;
         units.decode(u, s);
         const int ia = i_lo + s.ia, ib = i_lo + s.ib;
-        const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+        const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
         auto load_p0 = [&](int plane) {
           const int slot = sp % SP;
           if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
@@ -640,7 +640,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       if (u == kNoUnit) break;
       units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
-      const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+      const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
       const int j1 = j0 - 1 + r;
       const int kq = k0 - 4 + hl * 4;
       const bool row_in = j1 >= j_lo && j1 < j_hi;
@@ -715,7 +715,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       if (u == kNoUnit) break;
       units.decode(u, s);
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
-      const int k0 = s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+      const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
       const int j = j0 + r2;
       const int kq = k0 - 4 + hl * 4;
       const bool row_in = j < j_hi;
@@ -891,10 +891,18 @@ static int env_int(const char* name) {
   return e ? atoi(e) : -1;
 }
 
+// First output column of k-tile 0.  -4 puts every tile's coefficient boxes (origin
+// k0-4) on a 32-byte sector boundary: 8 sectors per 64-column row instead of 9
+// (HIMENO_TB2_KORG=0 restores tiles starting at column 0).
+static int tb2_k_org() {
+  static const int v = env_int("HIMENO_TB2_KORG") == 0 ? 0 : -4;
+  return v;
+}
+
 template <int LW, int NW1, int SC>
 static long long tb2_tiles(int nj, int k_hi) {
   using T = Tb2<LW, NW1, SC>;
-  return (long long)((k_hi + T::TK2 - 1) / T::TK2) * ((nj + T::TJ2 - 1) / T::TJ2);
+  return (long long)((k_hi - tb2_k_org() + T::TK2 - 1) / T::TK2) * ((nj + T::TJ2 - 1) / T::TJ2);
 }
 
 // Makespan of one pass: the device-wide queue hands the units (`full` whole
@@ -977,7 +985,8 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
                       int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
                       int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
   using T = Tb2<LW, NW1, SC>;
-  const int ktiles = (k_hi + T::TK2 - 1) / T::TK2;
+  const int k_org = tb2_k_org();
+  const int ktiles = (k_hi - k_org + T::TK2 - 1) / T::TK2;
   const int jtiles = (j_hi - j_lo + T::TJ2 - 1) / T::TJ2;
   const long long tiles = (long long)ktiles * jtiles;
   if (full < 0 || full > tiles) full = 0;
@@ -1006,8 +1015,8 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   cfg.attrs = la;
   cfg.numAttrs = pdl ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC>, maps, F, p_out, i_lo,
-                                           i_hi, j_lo, j_hi, k_lo, k_hi, ktiles, chunk, full, g_lo,
-                                           g_hi, a.omega, g, a.gosa_reset);
+                                           i_hi, j_lo, j_hi, k_lo, k_hi, k_org, ktiles, chunk, full,
+                                           g_lo, g_hi, a.omega, g, a.gosa_reset);
   return e == cudaSuccess ? 1 : -1;
 }
 

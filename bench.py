@@ -166,6 +166,15 @@ def dist_setup():
     return world, rank, local
 
 
+def host_threads() -> int:
+    """Host threads this process may run on (torchrun exports OMP_NUM_THREADS=1, which
+    must not shrink the CPU reference: rank 0 alone runs it)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return max(1, os.cpu_count() or 1)
+
+
 def cpu_baseline(size, seconds: float, threads: int) -> dict:
     """CPU oracle jacobi on the same grid, bounded to ~`seconds` of work."""
     from oracle import oracle
@@ -215,7 +224,7 @@ def run_reference(args, world, rank):
     from oracle import oracle
     from paper_2002_12115_b200.apps import himeno
     size = himeno.size(args.size)
-    threads = oracle.max_threads()
+    threads = host_threads()
     f = oracle.empty_fields(size.I, size.J, size.K)
     oracle.initmt(f)
     for _ in range(args.warmup):
@@ -522,8 +531,7 @@ def run_ours(args, world, rank, local):
                 "achieved_gbs": BYTES_STENCIL * osz.interior_points / (okt.stencil_ms / 1e3) / 1e9}
         extra["other_grids"] = others
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle
-        extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, oracle.max_threads())
+        extra["cpu_baseline"] = cpu_baseline(size, args.cpu_seconds, host_threads())
     if rank == 0 and not args.no_ga:
         # N > 1: the population is sharded over every GPU of the node (config 4), one
         # worker slot per GPU, from rank 0's process

@@ -407,7 +407,8 @@ def run_ours(args, world, rank, local):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": ("k_stencil_tb2 (temporal blocking: 2 iterations per pass, 56 B/pt "
-                           "per pass; warp-specialised TMA pipeline)"
+                           "per pass; warp-specialised TMA pipeline, step-2 coefficients "
+                           "stashed in tensor memory)"
                            if variant == 1 and kt.stencil_iters > 1.5 else "k_stencil_tma<3>"),
                 "bytes_per_point": BYTES_STENCIL, "points_per_launch": points,
                 "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,

@@ -261,17 +261,20 @@ def test_two_step_shapes_bit_exact(gpu, monkeypatch, shape, chunk):
     assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
 
 
+@pytest.mark.parametrize("stash", [0, 1])
 @pytest.mark.parametrize("full", [0, 2, 5, 9])
-def test_two_step_whole_columns_bit_exact(gpu, monkeypatch, full):
+def test_two_step_whole_columns_bit_exact(gpu, monkeypatch, full, stash):
     """Whole tile columns ahead of the chunked tail (HIMENO_TB2_FULL pins how many; the
     grid has 3 x 3 tiles of shape (16,8,4), so 9 = every tile a whole column) give the
-    same field, bit for bit, as the oracle."""
+    same field, bit for bit, as the oracle -- with the step-2 coefficients stashed in
+    tensor memory (the default) and read from the shared-memory stage."""
     sz = himeno.custom_size(75, 45, 141)
     nn = 4
     ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
     monkeypatch.setenv("HIMENO_TB2_SHAPE", "1")
     monkeypatch.setenv("HIMENO_TB2_CHUNK", "16")
     monkeypatch.setenv("HIMENO_TB2_FULL", str(full))
+    monkeypatch.setenv("HIMENO_TB2_STASH", str(stash))
     lib = N.load()
     old = lib.hp_set_temporal_blocking(1)
     try:

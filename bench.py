@@ -470,39 +470,43 @@ def run_ours(args, world, rank, local):
                              else "hp_write_field + hp_dd_jacobi + hp_read_field per slab (C ABI)")
     pipelined = None
     if slab is None and e2e_steps >= 2:
-        # two contexts, jobs alternate: one job's H2D overlaps the other's loop + D2H
-        ctx2 = N.Context(local, size.I, size.J, size.K)
-        ptr2 = ctx.lib.hp_host_alloc(nbytes)
-        if not ptr2:
-            raise RuntimeError("pinned allocation failed")
-        pinned.append(ptr2)
-        p_out2 = np.ctypeslib.as_array(
-            (ctypes.c_float * (nbytes // 4)).from_address(ptr2)).reshape(I_loc, size.J, size.K)
-        ctxs, outs = (ctx, ctx2), (p_out, p_out2)
+        # K contexts, jobs round-robin: while one job's inputs stream in over PCIe the
+        # others run their loops and read back, so the host->device link never idles
+        K = max(2, args.e2e_contexts)
+        ctxs, outs = [ctx], [p_out]
+        for _ in range(K - 1):
+            ctxs.append(N.Context(local, size.I, size.J, size.K))
+            ptr2 = ctx.lib.hp_host_alloc(nbytes)
+            if not ptr2:
+                raise RuntimeError("pinned allocation failed")
+            pinned.append(ptr2)
+            outs.append(np.ctypeslib.as_array(
+                (ctypes.c_float * (nbytes // 4)).from_address(ptr2)).reshape(I_loc, size.J, size.K))
         gosas = []
 
         def run_pipelined(n):
-            pending = [False, False]
+            pending = [False] * K
             for s in range(n):
-                x = s % 2
+                x = s % K
                 if pending[x]:
                     gosas.append(ctxs[x].sync())
                 ctxs[x].jacobi_host_async(host, nn, variant, outs[x])
                 pending[x] = True
-            for x in (0, 1):
+            for x in range(K):
                 if pending[x]:
                     gosas.append(ctxs[x].sync())
 
-        run_pipelined(2)   # warm-up of the second context
+        run_pipelined(K)   # warm-up of every context
         gosas.clear()
         pipe_s = timed(run_pipelined, e2e_steps)
-        if any(g != gosa_serial for g in gosas) or not np.array_equal(p_out, p_out2):
+        if any(g != gosa_serial for g in gosas) or not all(np.array_equal(p_out, o) for o in outs[1:]):
             raise RuntimeError("pipelined e2e results differ from the serial call")
-        ctx2.close()
+        for c in ctxs[1:]:
+            c.close()
         pipelined = pipe_s
         e2e_s = pipe_s
-        path = ("hp_jacobi_host_async on two contexts, jobs alternating (H2D of one job "
-                "overlaps the other's loop + D2H), pinned host")
+        path = (f"hp_jacobi_host_async on {K} contexts, jobs round-robin (H2D of one job "
+                "overlaps the others' loops + D2H), pinned host")
     for ptr in pinned:
         ctx.lib.hp_host_free(ptr)
     e2e_value = e2e_steps * flops_step / e2e_s / 1e9
@@ -585,6 +589,8 @@ def main(argv=None) -> int:
     ap.add_argument("--nn", type=int, default=100)
     ap.add_argument("--variant", type=int, default=1, choices=[0, 1])
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-contexts", type=int, default=2,
+                    help="contexts (jobs in flight) of the pipelined e2e measurement")
     ap.add_argument("--no-ga", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-grids", action="store_true")

@@ -1112,11 +1112,12 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
   static const double cost[kTb2Shapes] = {1.03, 1.005, 0.91, 0.885};
   const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_TB2_CHUNK");
   const int pin_full = env_int("HIMENO_TB2_FULL");
-  const bool pinned = pin_shape >= 0 || pin_chunk > 0 || pin_full >= 0;
+  // cached per geometry and pins (the list-scheduling model is too slow to rerun
+  // for every pass)
   static std::mutex mu;
-  static std::map<std::array<int, 4>, Tb2Choice> cache;
-  const std::array<int, 4> key{ni, nj, k_hi, sms};
-  if (!pinned) {
+  static std::map<std::array<int, 7>, Tb2Choice> cache;
+  const std::array<int, 7> key{ni, nj, k_hi, sms, pin_shape, pin_chunk, pin_full};
+  {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
@@ -1144,7 +1145,7 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
       }
     }
   }
-  if (!pinned) {
+  {
     std::lock_guard<std::mutex> lock(mu);
     cache[key] = best;
   }

@@ -29,6 +29,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // hardware-defined interval) is seconds, far beyond any legitimate wait.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
+#pragma unroll 1
   for (uint32_t n = 0; n < (1u << 26); ++n) {
     asm volatile(
         "{\n"

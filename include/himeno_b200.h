@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define HP_ABI_VERSION 1
+#define HP_ABI_VERSION 2
 
 /* ---- status codes ------------------------------------------------------ */
 enum hp_status {
@@ -117,7 +117,12 @@ enum hp_flags {
   HP_FLAG_POISON_DEVICE = 4,    /* fill device mirrors with NaN before the run      */
   HP_FLAG_KERNEL_TIMING = 8,    /* CUDA events around every launch (slower)         */
   HP_FLAG_GRAPH_TIME_LOOP = 16, /* replay the device time loop as a CUDA graph      */
-  HP_FLAG_FUSED_TIME_LOOP = 32  /* time loop: fused stencil with p/wrk2 rotation    */
+  HP_FLAG_FUSED_TIME_LOOP = 32, /* time loop: fused stencil with p/wrk2 rotation    */
+  HP_FLAG_LITERAL_GOSA = 64     /* verification: when the last iteration's stencil
+                                   runs on the device, its ss*ss terms are also
+                                   written out (side kernel on the same device
+                                   state) and summed in program order on the host
+                                   after the timed run -> gosa_f32 literal          */
 };
 
 typedef struct hp_schedule {
@@ -143,9 +148,16 @@ typedef struct hp_result {
   uint64_t n_implicit;              /* implicit present_or_copy transfers               */
   uint64_t n_launch;                /* kernels launched                                 */
   uint64_t n_stale_reads;           /* compute read a copy older than the other side    */
-  double gosa;            /* main's printed gosa: host copy after jacobi returns    */
+  double gosa;            /* jacobi's gosa, terms summed in fp64 (host copy at return) */
   float samples[HP_MAX_SAMPLES];    /* main's printed p samples (host copy)         */
   int32_t n_samples;
+  float gosa_f32;         /* main's printed float gosa: the program's literal fp32
+                             sequential sum when every ss*ss term of the last
+                             iteration was summed on the host, or with
+                             HP_FLAG_LITERAL_GOSA (gosa_f32_literal = 1); else
+                             (float)gosa -- a parallel device reduction has no
+                             sequential order to reproduce (B.5)      */
+  int32_t gosa_f32_literal;
   int32_t status;         /* hp_status                                              */
   char diag[256];
 } hp_result;
@@ -240,6 +252,12 @@ int hp_nccl_unique_id(unsigned char* out, size_t n);
 int hp_dd_init(hp_ctx* ctx, int nranks, int rank, const unsigned char* id, size_t n);
 int hp_dd_jacobi(hp_ctx* ctx, int nn);
 int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
+
+/* Diagnostics: the dynamic shared-memory limit (bytes) the large-shared-memory
+ * kernel `id` has in `device`'s context (0..2 single-step stencil with 2..4
+ * stages, 3..6 two-step shapes, 7 two-step with the tensor-memory stash).  The
+ * library raises it per device before the first launch there. */
+int hp_smem_optin(int id, int device, int* bytes);
 
 /* Pinned host buffers for callers without their own allocator (e2e inputs). */
 void* hp_host_alloc(size_t bytes);

@@ -43,6 +43,7 @@ struct hp_ctx {
   // [i_off, i_off + I) of a gI-plane grid; stencil interior = local [li_lo, li_hi)
   int gI = 0, i_off = 0, li_lo = 1, li_hi = 0;
   void* dd = nullptr;            // decomposition state (NCCL communicator, ...)
+  float* terms = nullptr;        // HP_FLAG_LITERAL_GOSA: last iteration's ss*ss, [I][J][K]
 
   hp::GosaSink sink() const {
     hp::GosaSink g;

@@ -193,6 +193,7 @@ extern "C" void hp_destroy(hp_ctx* c) {
   if (c->dscal) cudaFree(c->dscal);
   if (c->partials) cudaFree(c->partials);
   if (c->ticket) cudaFree(c->ticket);
+  if (c->terms) cudaFree(c->terms);
   for (float* h : c->host)
     if (h) cudaFreeHost(h);
   if (c->hscal) cudaFreeHost(c->hscal);
@@ -366,9 +367,12 @@ static void host_stencil_row(const float* __restrict__ p, const float* __restric
   }
 }
 
-static double host_stencil(const HostFields& H, const Box& b, float omega) {
+// Returns the fp64 sum of the box's ss*ss terms; *lit32 continues the program's
+// literal fp32 sequential sum (`gosa += ss*ss` with float gosa) over the same terms.
+static double host_stencil(const HostFields& H, const Box& b, float omega, float* lit32) {
   const int n = b.k1 - b.k0;
   if (n <= 0) return 0.0;
+  float g32 = *lit32;
   const size_t R = (size_t)H.K, L = (size_t)H.J * H.K;
   std::vector<float> t((size_t)n);
   double acc = 0.0;
@@ -382,8 +386,12 @@ static double host_stencil(const HostFields& H, const Box& b, float omega) {
                        H.f[HP_F_C0] + c, H.f[HP_F_C1] + c, H.f[HP_F_C2] + c,
                        H.f[HP_F_WRK1] + c, H.f[HP_F_BND] + c, H.f[HP_F_WRK2] + c, t.data(), n,
                        R, L, omega);
-      for (int k = 0; k < n; ++k) acc += (double)t[k];   // k order, as the program
+      for (int k = 0; k < n; ++k) {   // k order, as the program
+        acc += (double)t[k];
+        g32 += t[k];
+      }
     }
+  *lit32 = g32;
   return acc;
 }
 
@@ -409,6 +417,13 @@ struct Runner {
   double t_start = 0, deadline = 0;
   bool guard = true;
   bool pending_h2d = false;
+  // the program's literal fp32 gosa: valid while every ss*ss term since the
+  // last `gosa = 0.0` was summed on the host, in program order
+  float lit32 = 0.0f;
+  bool lit_valid = false;
+  // HP_FLAG_LITERAL_GOSA: the last iteration's device-side terms (C->terms)
+  bool literal = false, terms_valid = false;
+  int cur_iter = -1;               // host time loop: current iteration of loop 6
   int status = HP_OK;
   char diag[256] = {0};
 
@@ -674,8 +689,18 @@ struct Runner {
     for (int v : imp) h2d(v, true);
     if (failed()) return;
     note_device_access(nest, b);
+    int n = 0;
+    if (nest == NEST_STENCIL) {
+      lit_valid = false;   // terms summed on the device
+      if (literal && cur_iter == C->hs<int>(HP_V_NN) - 1) {
+        if (launch_stencil_terms(C->dev, C->dev.f[HP_F_P], C->terms, b, C->stream) < 0) {
+          fail(HP_FAIL_LAUNCH, "terms kernel: %s", cudaGetErrorString(cudaGetLastError()));
+          return;
+        }
+        terms_valid = true;
+      }
+    }
     const LaunchArgs a = args(0);
-    int n;
     if (full_tuned && map == MAP_COLLAPSE && nest == NEST_STENCIL)
       n = launch_stencil_3d(C->dev, a, C->sink(), C->stream);
     else if (full_tuned && map == MAP_COLLAPSE && nest == NEST_COPY)
@@ -721,7 +746,7 @@ struct Runner {
       case NEST_INIT1: host_init1(H, b, C->hs<int>(HP_V_IMAX)); break;
       case NEST_STENCIL: {
         host_read(HP_V_GOSA);
-        C->hs<double>(HP_V_GOSA) += host_stencil(H, b, C->hs<float>(HP_V_OMEGA));
+        C->hs<double>(HP_V_GOSA) += host_stencil(H, b, C->hs<float>(HP_V_OMEGA), &lit32);
         host_write(HP_V_GOSA);
         break;
       }
@@ -780,18 +805,27 @@ struct Runner {
     if (failed()) return;
     const int nn = C->hs<int>(HP_V_NN);
     const int k6 = kind(6);
+    if (nn > 0) lit_valid = false;
     const bool fused = (S->flags & HP_FLAG_FUSED_TIME_LOOP) && k6 != HP_K_PLV;
     const Box interior = nest_box(NEST_STENCIL);
     if (nn > 0) note_device_access(NEST_STENCIL, interior);
     int n = 0;
     if (nn > 0) {
+      float* terms = literal ? C->terms : nullptr;
       if (fused) {
-        n = time_loop_fused(C, nn, args(1));
+        n = time_loop_fused(C, nn, args(1), terms, interior);
       } else {
         const Box bs = nest_box(NEST_STENCIL);
         for (int it = 0; it < nn && n >= 0; ++it) {
           const LaunchArgs a = args(1);
           int r1, r2;
+          if (terms && it == nn - 1) {
+            if (launch_stencil_terms(C->dev, C->dev.f[HP_F_P], terms, bs, C->stream) < 0) {
+              n = -1;
+              break;
+            }
+            n += 1;
+          }
           if (k6 == HP_K_PLV) {
             r1 = launch_nest(NEST_STENCIL, MAP_VECTOR, C->dev, bs, a, C->sink(), C->stream);
             r2 = launch_nest(NEST_COPY, MAP_VECTOR, C->dev, bs, a, C->sink(), C->stream);
@@ -807,6 +841,7 @@ struct Runner {
       fail(HP_FAIL_LAUNCH, "time-loop launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       return;
     }
+    if (literal && nn > 0) terms_valid = true;
     R->n_launch += (uint64_t)n;
     C->launches += (uint64_t)n;
     if (nn > 0) {
@@ -822,15 +857,33 @@ struct Runner {
 
  public:
   // the fused device time loop: one- and two-step passes (temporal blocking)
-  static int time_loop_fused(hp_ctx* c, int nn, const LaunchArgs& a) {
+  // With `terms` (verification mode) the passes stop before the last iteration,
+  // whose ss*ss terms are written out from the rotation buffer holding p_{nn-1}.
+  static int time_loop_fused(hp_ctx* c, int nn, const LaunchArgs& a, float* terms = nullptr,
+                             const Box& interior = Box{}) {
     int n = 0, r;
     if ((r = time_loop_begin(c, a)) < 0) return -1;
     n += r;
     float* last = nullptr;
-    if ((r = stencil_iterations(c->dev, c->dev.f[HP_F_P], c->scratch, nn, a, c->sink(),
-                                c->stream, &last, nullptr)) < 0)
-      return -1;
-    n += r;
+    if (!terms) {
+      if ((r = stencil_iterations(c->dev, c->dev.f[HP_F_P], c->scratch, nn, a, c->sink(),
+                                  c->stream, &last, nullptr)) < 0)
+        return -1;
+      n += r;
+    } else {
+      float* mid = nullptr;
+      if ((r = stencil_iterations(c->dev, c->dev.f[HP_F_P], c->scratch, nn - 1, a, c->sink(),
+                                  c->stream, &mid, nullptr)) < 0)
+        return -1;
+      n += r;
+      if ((r = launch_stencil_terms(c->dev, mid, terms, interior, c->stream)) < 0) return -1;
+      n += r;
+      float* other = mid == c->dev.f[HP_F_P] ? c->scratch : c->dev.f[HP_F_P];
+      if ((r = stencil_iterations(c->dev, mid, other, 1, a, c->sink(), c->stream, &last,
+                                  nullptr)) < 0)
+        return -1;
+      n += r;
+    }
     if ((r = time_loop_finish(c, last, a)) < 0) return -1;
     return n + r;
   }
@@ -842,8 +895,12 @@ struct Runner {
     } else {
       const int nn = C->hs<int>(HP_V_NN);
       for (int it = 0; it < nn && !failed(); ++it) {
+        cur_iter = it;
         C->hs<double>(HP_V_GOSA) = 0.0;  // gosa = 0.0;  (host statement in loop 6)
         host_write(HP_V_GOSA);
+        lit32 = 0.0f;
+        lit_valid = true;
+        terms_valid = false;
         run_nest(NEST_STENCIL);
         run_nest(NEST_COPY);
         check_time();
@@ -913,6 +970,27 @@ struct Runner {
     return HP_OK;
   }
 
+  // Verification mode, after the timed run: the device-side terms of the last
+  // iteration summed as the program does (`gosa += ss*ss`, float, i/j/k order).
+  void finish_literal() {
+    if (failed() || !literal || lit_valid || !terms_valid) return;
+    const Box b = nest_box(NEST_STENCIL);
+    std::vector<float> t((size_t)C->I * C->J * C->K);
+    if (!cuda_ok(cudaMemcpyAsync(t.data(), C->terms, t.size() * sizeof(float),
+                                 cudaMemcpyDeviceToHost, C->stream), "terms D2H") ||
+        !cuda_ok(cudaStreamSynchronize(C->stream), "terms sync"))
+      return;
+    const HostFields H = C->hostf();
+    float g = 0.0f;
+    for (int i = b.i0; i < b.i1; ++i)
+      for (int j = b.j0; j < b.j1; ++j) {
+        const float* row = t.data() + H.at(i, j, 0);
+        for (int k = b.k0; k < b.k1; ++k) g += row[k];
+      }
+    R->gosa_f32 = g;
+    R->gosa_f32_literal = 1;
+  }
+
   void reset_state() {
     C->clock = 1;
     for (int v = 0; v < HP_NVARS; ++v) {
@@ -944,6 +1022,8 @@ struct Runner {
     // main:gosa = jacobi's return value (host copy); printed with the p samples
     host_read(HP_V_GOSA);
     R->gosa = C->hs<double>(HP_V_GOSA);
+    R->gosa_f32_literal = lit_valid ? 1 : 0;
+    R->gosa_f32 = lit_valid ? lit32 : (float)R->gosa;
     host_read(HP_V_P);
     const int ns = (int)C->samples.size() / 3;
     R->n_samples = ns;
@@ -968,6 +1048,7 @@ extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
   run.S = s;
   run.R = r;
   run.guard = (s->flags & HP_FLAG_COHERENCE_GUARD) != 0;
+  run.literal = (s->flags & HP_FLAG_LITERAL_GOSA) != 0;
   int rc = run.prepare();
   if (rc != HP_OK) return rc;
   if (run.failed()) {  // rejected pattern: nothing executes
@@ -998,6 +1079,10 @@ extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
     if (launch_fill(c->slab, c->field_stride * (HP_NFIELDS + 1), nanf(""), c->stream) < 0)
       return cuda_fail(cudaGetLastError(), "poison");
   }
+  if (run.literal && !c->terms) {
+    e = cudaMalloc(&c->terms, (size_t)c->I * c->J * c->K * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(terms)");
+  }
   cudaMemsetAsync(c->dscal, 0xff, HP_NVARS * SLOT_BYTES, c->stream);
   e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(e, "pre-run sync");
@@ -1008,6 +1093,7 @@ extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
   run.program();
   if (run.status == HP_TIMEOUT || run.status == HP_FAIL_LAUNCH) cudaStreamSynchronize(c->stream);
   r->wall_s = now_s() - run.t_start;
+  run.finish_literal();   // verification mode only; not part of the timed run
   // a sticky device error (illegal address, ...) poisons the context
   e = cudaGetLastError();
   if (e != cudaSuccess && run.status == HP_OK)

@@ -86,6 +86,9 @@ int launch_copy_3d(const DevFields& F, const LaunchArgs& a, cudaStream_t s);
 int launch_stencil_rotate(const DevFields& F, const float* p_in, float* p_out,
                           const LaunchArgs& a, const GosaSink& g, cudaStream_t s);
 int launch_fill(float* dst, size_t n, float value, cudaStream_t s);
+// ss*ss of each point of box b (stencil over p) -> terms[(i*J + j)*K + k]
+int launch_stencil_terms(const DevFields& F, const float* p, float* terms, const Box& b,
+                         cudaStream_t s);
 // dst[r*dpitch + c] = src[r*spitch + c] for r < rows, c < width (elements)
 int launch_repitch(float* dst, size_t dpitch, const float* src, size_t spitch, int width,
                    size_t rows, cudaStream_t s);
@@ -113,6 +116,12 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
 int stencil_iterations(const DevFields& F, float* buf0, float* buf1, int nn, const LaunchArgs& a,
                        const GosaSink& g, cudaStream_t s, float** last, int* stencil_launches);
 int set_temporal_blocking(int on);
+// raise a kernel's dynamic shared-memory limit on the current device (once per
+// kernel and device); false if the runtime refuses
+bool ensure_smem_optin(const void* func, int bytes);
+const void* smem_kernel(int id);   // the opted-in kernels by id (hp_smem_optin)
+void set_error(const char* fmt, ...);   // executor.cpp: hp_last_error() text
+int cuda_fail(cudaError_t e, const char* what);
 
 // ---- host loop bodies (executor.cpp), same arithmetic as the kernels --------
 struct HostFields {

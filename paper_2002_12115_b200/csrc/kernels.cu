@@ -406,6 +406,36 @@ __global__ void k_fill(float* dst, size_t n, float v) {
     dst[t] = v;
 }
 
+// Verification mode (HP_FLAG_LITERAL_GOSA): the ss*ss terms of one stencil
+// execution over box b, from the same device state and with the same arithmetic
+// as the stencil kernel about to run, stored at their program-order position
+// [i][j][k] of an unpadded I x J x K buffer (the host sums them sequentially).
+__global__ void k_stencil_terms(DevFields F, const float* __restrict__ p, float* __restrict__ terms,
+                                Box b) {
+  const long long nk = b.nk(), nj = b.nj(), total = b.count();
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = b.k0 + (int)(t % nk);
+    const int j = b.j0 + (int)((t / nk) % nj);
+    const int i = b.i0 + (int)(t / (nk * nj));
+    const size_t c = F.at(i, j, k);
+    const size_t P = F.P, L = F.plane();
+    Coef q;
+    q.a0 = F.f[HP_F_A0][c]; q.a1 = F.f[HP_F_A1][c]; q.a2 = F.f[HP_F_A2][c];
+    q.a3 = F.f[HP_F_A3][c]; q.b0 = F.f[HP_F_B0][c]; q.b1 = F.f[HP_F_B1][c];
+    q.b2 = F.f[HP_F_B2][c]; q.c0 = F.f[HP_F_C0][c]; q.c1 = F.f[HP_F_C1][c];
+    q.c2 = F.f[HP_F_C2][c]; q.wrk1 = F.f[HP_F_WRK1][c]; q.bnd = F.f[HP_F_BND][c];
+    const float n[19] = {
+        p[c + L], p[c + P], p[c + 1],
+        p[c + L + P], p[c + L - P], p[c - L + P], p[c - L - P],
+        p[c + P + 1], p[c - P + 1], p[c + P - 1], p[c - P - 1],
+        p[c + L + 1], p[c - L + 1], p[c + L - 1], p[c - L - 1],
+        p[c - L], p[c - P], p[c - 1], p[c]};
+    const float ss = stencil_ss(q, n);
+    terms[((size_t)i * F.J + j) * F.K + k] = mul(ss, ss);
+  }
+}
+
 template <int NEST>
 int launch_nest_t(Mapping map, const DevFields& F, const Box& b, const LaunchArgs& a,
                   const GosaSink& g, cudaStream_t s) {
@@ -611,6 +641,15 @@ int launch_repitch(float* dst, size_t dpitch, const float* src, size_t spitch, i
 
 int launch_fill(float* dst, size_t n, float value, cudaStream_t s) {
   k_fill<<<sm_count() * 8, 256, 0, s>>>(dst, n, value);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_stencil_terms(const DevFields& F, const float* p, float* terms, const Box& b,
+                         cudaStream_t s) {
+  if (b.count() <= 0) return 0;
+  const long long need = (b.count() + 255) / 256;
+  const int blocks = (int)(need < (long long)sm_count() * 16 ? need : (long long)sm_count() * 16);
+  k_stencil_terms<<<blocks, 256, 0, s>>>(F, p, terms, b);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

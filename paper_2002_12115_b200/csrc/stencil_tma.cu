@@ -1006,6 +1006,43 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
 
 void destroy_stencil_tma(void* h) { delete static_cast<TmaState*>(h); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) changes the kernel in the
+// *current device's* context only, so the opt-in is recorded per (kernel, device):
+// a process that drives several GPUs (B200Evaluator over every device,
+// hp_group_jacobi) raises it on each device before the first launch there.
+bool ensure_smem_optin(const void* func, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;   // (kernel, device) -> bytes
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return true;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  have = bytes;
+  return true;
+}
+
+// The large-shared-memory kernels by id (hp_smem_optin): 0..2 = single-step with
+// 2..4 stages, 3.. = two-step shapes 0..3, 7 = shape 1 with the tensor-memory stash.
+const void* smem_kernel(int id) {
+  switch (id) {
+    case 0: return (const void*)k_stencil_tma<2>;
+    case 1: return (const void*)k_stencil_tma<3>;
+    case 2: return (const void*)k_stencil_tma<4>;
+    case 3: return (const void*)k_stencil_tb2<32, 8, 4, false>;
+    case 4: return (const void*)k_stencil_tb2<16, 8, 4, false>;
+    case 5: return (const void*)k_stencil_tb2<16, 6, 5, false>;
+    case 6: return (const void*)k_stencil_tb2<16, 5, 6, false>;
+    case 7: return (const void*)k_stencil_tb2<16, 8, 4, true>;
+    default: return nullptr;
+  }
+}
+
 // Launch the TMA stencil with S stages; returns 1, 0 (not applicable: caller
 // falls back), or -1 on launch error.
 int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, float* p_out,
@@ -1028,14 +1065,10 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
   const size_t smem = 128 + (size_t)stages * kStageBytes + 2 * stages * sizeof(uint64_t) +
                       sizeof(UnitRing);
   // the work-queue counter is zero: set at context creation, reset by the last CTA
-  static bool attr_set[5] = {};   // per stage count: raise the dynamic smem limit once
+  bool attr_ok = true;
   auto launch = [&](auto kern) {
-    if (!attr_set[stages]) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-        return;
-      attr_set[stages] = true;
-    }
+    // the opt-in is a property of the kernel in the current device's context
+    if (!(attr_ok = ensure_smem_optin((const void*)kern, (int)smem))) return;
     kern<<<(int)grid, kThreads, smem, s>>>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
                                            ktiles, chunk, a.omega, g, a.gosa_reset);
   };
@@ -1045,6 +1078,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
     case 4: launch(k_stencil_tma<4>); break;
     default: return 0;
   }
+  if (!attr_ok) return -1;
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -1107,16 +1141,17 @@ struct Tb2Choice {
   int shape, chunk, full;
 };
 static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
-  // (16,8,4) runs with the tensor-memory stash: 3.5 % faster per plane step than the
-  // 1.04 measured without it
-  static const double cost[kTb2Shapes] = {1.03, 1.005, 0.91, 0.885};
+  // (16,8,4) runs with the tensor-memory stash unless HIMENO_TB2_STASH=0: 1.005 us
+  // per plane step with it, 1.04 without
+  const bool stash = env_int("HIMENO_TB2_STASH") != 0;
+  const double cost[kTb2Shapes] = {1.03, stash ? 1.005 : 1.04, 0.91, 0.885};
   const int pin_shape = env_int("HIMENO_TB2_SHAPE"), pin_chunk = env_int("HIMENO_TB2_CHUNK");
   const int pin_full = env_int("HIMENO_TB2_FULL");
-  // cached per geometry and pins (the list-scheduling model is too slow to rerun
-  // for every pass)
+  // cached per geometry, pins and stash setting (the list-scheduling model is too
+  // slow to rerun for every pass)
   static std::mutex mu;
-  static std::map<std::array<int, 7>, Tb2Choice> cache;
-  const std::array<int, 7> key{ni, nj, k_hi, sms, pin_shape, pin_chunk, pin_full};
+  static std::map<std::array<int, 8>, Tb2Choice> cache;
+  const std::array<int, 8> key{ni, nj, k_hi, sms, pin_shape, pin_chunk, pin_full, (int)stash};
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
@@ -1168,13 +1203,7 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   if (units > g.capacity) return -1;   // one gosa partial per unit
   const size_t smem = T::smem_bytes();
   // the work-queue counter is zero: set at context creation, reset by the last CTA
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_stencil_tb2<LW, NW1, SC, ST>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  if (!ensure_smem_optin((const void*)k_stencil_tb2<LW, NW1, SC, ST>, (int)smem)) return -1;
   static const bool pdl = env_int("HIMENO_TB2_PDL") != 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute la[1];
@@ -1227,3 +1256,22 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
 }
 
 }  // namespace hp
+
+// Diagnostics: the dynamic shared-memory limit kernel `id` has on `device`
+// (cudaFuncGetAttributes in that device's context).
+extern "C" int hp_smem_optin(int id, int device, int* bytes) {
+  const void* f = hp::smem_kernel(id);
+  if (!f || !bytes) {
+    hp::set_error("hp_smem_optin: bad arguments");
+    return HP_ERR_ARG;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  cudaFuncAttributes fa{};
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return hp::cuda_fail(e, "hp_smem_optin");
+  *bytes = fa.maxDynamicSharedSizeBytes;
+  return HP_OK;
+}

@@ -121,6 +121,7 @@ class B200Evaluator:
         self._low_lock = threading.Lock()
         self.stats: dict = {}          # genome -> native result stats of its last run
         self._last_slot = 0
+        self._count_lock = threading.Lock()   # measure() runs on run_ga's pool threads
         self.evaluations = 0
 
     # -- construction from the reference pipeline objects ----------------------
@@ -175,55 +176,82 @@ class B200Evaluator:
         with ThreadPoolExecutor(max_workers=len(missing)) as pool:
             list(pool.map(self._context, missing))
 
-    def _execute(self, genome):
+    def _execute(self, genome, extra_flags: int = 0):
+        """Run once in a leased worker slot; returns (lowered, result, slot)."""
         low = self.lowered(genome)
         if low.failure is not None:
-            return low, None
+            return low, None, None
+        sched = low.schedule
+        if extra_flags:
+            sched = N.Schedule.from_buffer_copy(low.schedule)   # events stay owned by `low`
+            sched.flags |= int(extra_flags)
         slot = self._free.get()
         try:
-            res = self._context(slot).run(low.schedule)
-            self._last_slot = slot
+            res = self._context(slot).run(sched)
         finally:
             self._free.put(slot)
-        return low, res
+        with self._count_lock:
+            self._last_slot = slot
+        return low, res, slot
 
     # -- plugin API ----------------------------------------------------------------------
     def measure(self, genome) -> MeasuredTime:
         genome = tuple(int(b) for b in genome)
-        low, res = self._execute(genome)
+        low, res, slot = self._execute(genome)
         if low.failure is not None:
             return MeasuredTime.failed(low.failure)
-        self.stats[genome] = res.stats()
-        self.evaluations += 1
+        st = res.stats()
+        st["slot"] = slot
+        st["device"] = self.devices[slot]
+        with self._count_lock:
+            self.stats[genome] = st
+            self.evaluations += 1
         if res.status == N.HP_OK:
             return MeasuredTime.ok(max(res.wall_s, 1e-9))
         if res.status == N.HP_TIMEOUT:
             return MeasuredTime.timeout()
         return MeasuredTime.failed(res.diag.decode(errors="replace") or f"status {res.status}")
 
-    def run(self, genome):
-        """Execute once and return the native result (raises on pattern failure)."""
+    def run(self, genome, with_slot: bool = False, literal_gosa: bool = False):
+        """Execute once and return the native result (raises on pattern failure);
+        with_slot: (result, worker slot whose context holds the run's fields);
+        literal_gosa: verification mode (HP_FLAG_LITERAL_GOSA, see run_for_output)."""
         genome = tuple(int(b) for b in genome)
-        low, res = self._execute(genome)
+        low, res, slot = self._execute(genome, N.FLAG_LITERAL_GOSA if literal_gosa else 0)
         if low.failure is not None:
             raise BaselineFailure(low.failure)
         if res.status != N.HP_OK:
             raise BaselineFailure(res.diag.decode(errors="replace"))
-        self.stats[genome] = res.stats()
-        return res
+        with self._count_lock:
+            self.stats[genome] = res.stats()
+        return (res, slot) if with_slot else res
 
-    def run_for_output(self, genome) -> str:
-        """The program's stdout for this pattern (main's printf lines, evaluators.py:183-188)."""
-        res = self.run(genome)
-        import numpy as np
-        lines = [f"{float(np.float32(res.gosa)):.9e}"]
+    def run_for_output(self, genome, literal_gosa: bool = True) -> str:
+        """The program's stdout for this pattern (main's printf lines, evaluators.py:183-188).
+
+        main prints its float gosa.  When the stencil's ss*ss terms are summed on the
+        host that is the literal fp32 sequential sum.  When they are summed on the
+        device, verification mode (``literal_gosa``, the default here: this is the
+        verification path, not a fitness measurement) also writes the last
+        iteration's terms out from the pattern's own device state and sums them in
+        program order, so the printed value is comparable token for token with the
+        original program's; with ``literal_gosa=False`` it is the fp32 rounding of
+        the device's fp64 reduction (2.6 % off the sequential fp32 sum at M, which
+        drifts: SURVEY.md §7.3)."""
+        res = self.run(genome, literal_gosa=literal_gosa)
+        lines = [f"{float(res.gosa_f32):.9e}"]
         lines += [f"{float(v):.9e}" for v in res.samples[:res.n_samples]]
         return "\n".join(lines) + "\n"
 
     def read_field(self, name: str, slot: Optional[int] = None, side: int = 0):
         """Host (side 0) or device (1) copy of a field after the last run in a worker slot
-        (default: the slot of the most recent run)."""
-        return self._context(self._last_slot if slot is None else slot).read_field(name, side)
+        (default: the slot of the most recent run -- pass the slot from
+        ``run(..., with_slot=True)`` or ``stats[genome]["slot"]`` when measuring
+        concurrently)."""
+        if slot is None:
+            with self._count_lock:
+                slot = self._last_slot
+        return self._context(slot).read_field(name, side)
 
     def close(self) -> None:
         with self._ctx_lock:

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import DeviceError, NativeUnavailable, TunerError
 
 LIB_PATH = Path(__file__).resolve().parent / "_native" / "libhimeno_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enums mirrored from include/himeno_b200.h ---------------------------------
 HP_OK, HP_FAIL_PATTERN, HP_FAIL_LAUNCH, HP_TIMEOUT, HP_FAIL_PRESENT = 0, 1, 2, 3, 4
@@ -37,6 +37,7 @@ FLAG_POISON_DEVICE = 4
 FLAG_KERNEL_TIMING = 8
 FLAG_GRAPH_TIME_LOOP = 16
 FLAG_FUSED_TIME_LOOP = 32
+FLAG_LITERAL_GOSA = 64
 MAX_SAMPLES = 8
 SLAB_HALO = 2      # halo planes per side of a slab context (csrc/decomp.cpp kHalo)
 
@@ -64,7 +65,9 @@ class Result(C.Structure):
                 ("n_skipped_stale", C.c_uint64), ("n_implicit", C.c_uint64),
                 ("n_launch", C.c_uint64), ("n_stale_reads", C.c_uint64),
                 ("gosa", C.c_double), ("samples", C.c_float * MAX_SAMPLES),
-                ("n_samples", C.c_int32), ("status", C.c_int32), ("diag", C.c_char * 256)]
+                ("n_samples", C.c_int32), ("gosa_f32", C.c_float),
+                ("gosa_f32_literal", C.c_int32), ("status", C.c_int32),
+                ("diag", C.c_char * 256)]
 
     def stats(self) -> dict:  # noqa: D401 - plain accessor
         return {"wall_s": self.wall_s, "host_s": self.host_s, "xfer_s": self.xfer_s,
@@ -72,7 +75,9 @@ class Result(C.Structure):
                 "n_h2d": self.n_h2d, "n_d2h": self.n_d2h,
                 "n_skipped_stale": self.n_skipped_stale, "n_implicit": self.n_implicit,
                 "n_launch": self.n_launch, "n_stale_reads": self.n_stale_reads,
-                "gosa": self.gosa, "samples": list(self.samples[:self.n_samples]),
+                "gosa": self.gosa, "gosa_f32": self.gosa_f32,
+                "gosa_f32_literal": bool(self.gosa_f32_literal),
+                "samples": list(self.samples[:self.n_samples]),
                 "status": self.status, "diag": self.diag.decode(errors="replace")}
 
 
@@ -115,6 +120,7 @@ SIGNATURES = {
     "hp_dd_init": (C.c_int, [_CtxP, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
     "hp_dd_jacobi": (C.c_int, [_CtxP, C.c_int]),
     "hp_dd_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "hp_smem_optin": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "hp_host_alloc": (C.c_void_p, [C.c_size_t]),
     "hp_host_free": (None, [C.c_void_p]),
 }
@@ -163,6 +169,13 @@ def group_jacobi(contexts, nn: int) -> float:
     g = C.c_double()
     check(load().hp_group_jacobi(arr, len(contexts), nn, C.byref(g)), "hp_group_jacobi")
     return g.value
+
+
+def smem_optin(kernel_id: int, device: int) -> int:
+    """Dynamic shared-memory limit (bytes) of a large-smem kernel on a device."""
+    out = C.c_int()
+    check(load().hp_smem_optin(kernel_id, device, C.byref(out)), "hp_smem_optin")
+    return out.value
 
 
 def last_error() -> str:

@@ -114,12 +114,13 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
     echo(f"best genome {ga.genome_str(best.genome)} time {best.time_s:.6g} s "
          f"ratio {ratio:.3f}x ({result.evaluations} evaluations)")
     if best.eval_source == "penalty" or best.timed_out:
-        # every evaluated pattern failed or timed out: nothing to verify (the reference
-        # would abort in run_for_output with BaselineFailure, cli.py:265 / evaluators.py:187)
-        verification = {"status": "skipped",
+        # every evaluated pattern failed or timed out: nothing ran to verify.  The
+        # reference aborts here (run_for_output raises BaselineFailure, cli.py:265 /
+        # evaluators.py:187); the run is reported, but as not passed (exit code 3)
+        verification = {"status": "no-runnable-pattern",
                         "reason": f"best individual did not run: {best.diagnostic or 'timeout'}"}
-        passed = True
-        echo("verification: skipped (no runnable pattern was evaluated)")
+        passed = False
+        echo("verification: FAIL (no runnable pattern was evaluated)")
     else:
         base_out = evaluator.run_for_output((0,) * gene_len)
         tuned_out = evaluator.run_for_output(best.genome)
@@ -161,6 +162,33 @@ def run_tuning(evaluator: B200Evaluator, config: ga.GAConfig, out_dir=None,
     return report, passed
 
 
+# device memory one B200 can give evaluator contexts (of ~180 GB; headroom for
+# the runtime, the scratch rotation buffer and other tenants)
+DEVICE_BYTES_FOR_CONTEXTS = 150e9
+MAX_AUTO_WORKERS = 8
+
+
+def auto_workers(size: str, n_dev: int, cpus: int) -> int:
+    """`--workers-per-device auto`: host cores per GPU, capped so the contexts fit in
+    device memory (each holds 15 pitched fields: L ~2 GB, XL ~16.3 GB) and in host
+    pinned memory, and by a small constant (more concurrent runs than that only
+    contend for the host cores and the PCIe link)."""
+    from .apps import himeno
+    sz = himeno.size(size)
+    pitch = -(-(sz.K + 4) // 32) * 32
+    per_ctx_dev = 15 * sz.I * sz.J * pitch * 4
+    per_ctx_host = 14 * sz.I * sz.J * sz.K * 4
+    by_cores = max(1, cpus // max(1, n_dev))
+    by_mem = max(1, int(DEVICE_BYTES_FOR_CONTEXTS // per_ctx_dev))
+    try:
+        import os
+        host_bytes = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        by_host = max(1, int(0.5 * host_bytes // (per_ctx_host * max(1, n_dev))))
+    except (ValueError, OSError, AttributeError):
+        by_host = MAX_AUTO_WORKERS
+    return max(1, min(by_cores, by_mem, by_host, MAX_AUTO_WORKERS))
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description="GA offload search on B200s")
     ap.add_argument("--app", default=None,
@@ -183,7 +211,7 @@ def main(argv=None) -> int:
         import os
         from . import native
         n_dev = native.device_count() if devices == "all" else len(devices)
-        workers = max(1, (os.cpu_count() or 1) // max(1, n_dev))
+        workers = auto_workers(args.size, n_dev, os.cpu_count() or 1)
     else:
         workers = int(args.workers_per_device)
     cfg = ga.GAConfig(population=args.population, generations=args.generations,

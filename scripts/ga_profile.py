@@ -43,20 +43,19 @@ def main():
                 with lock:
                     rows.append({"g": ga.genome_str(genome), "lower_ms": (t1 - t0) * 1e3,
                                  "failed": True, "t": t0})
-                return low, None
+                return low, None, None
             slot = ev._free.get()
             try:
                 t2 = time.perf_counter()
                 res = ev._context(slot).run(low.schedule)
                 t3 = time.perf_counter()
-                ev._last_slot = slot
             finally:
                 ev._free.put(slot)
             with lock:
                 rows.append({"g": ga.genome_str(genome), "lower_ms": (t1 - t0) * 1e3,
                              "wait_ms": (t2 - t1) * 1e3, "hp_run_ms": (t3 - t2) * 1e3,
                              "wall_ms": res.wall_s * 1e3, "t": t0, "slot": slot})
-            return low, res
+            return low, res, slot
 
         ev._execute = execute
         t0 = time.perf_counter()

@@ -16,7 +16,10 @@ for p in (str(ROOT),):
     if p not in sys.path:
         sys.path.insert(0, p)
 
-REFERENCE_SRC = Path("/root/reference/pkg/src")
+# the reference package: its sources in the dev container, else the unmodified
+# install build() puts into baseline/_ref (travels to the GPU box)
+REFERENCE_SRC = next((p for p in (Path("/root/reference/pkg/src"), ROOT / "baseline" / "_ref")
+                      if (p / "acctuner" / "ga.py").exists()), Path("/root/reference/pkg/src"))
 
 
 def pytest_configure(config):
@@ -44,9 +47,9 @@ def gpu():
 
 @pytest.fixture(scope="session")
 def reference():
-    """The reference package (dev container only)."""
+    """The reference package (sources here, baseline/_ref on the GPU box)."""
     if not REFERENCE_SRC.exists():
-        pytest.skip("reference not mounted")
+        pytest.skip("reference not available (run __graft_entry__.build())")
     if str(REFERENCE_SRC) not in sys.path:
         sys.path.insert(0, str(REFERENCE_SRC))
     import acctuner  # noqa: F401

@@ -385,3 +385,145 @@ def test_device_jacobi_zero_iterations(gpu, tb):
             assert np.array_equal(ctx.read_field("p", 1), ref["fields"]["p"])
     finally:
         lib.hp_set_temporal_blocking(old)
+
+
+# --- main's printed float gosa (hp_result.gosa_f32) ---------------------------------------
+
+GOLDEN_STDOUT = [("XXS", 1), ("XXS", 3), ("XS", 1), ("XS", 3), ("S", 2), ("M", 2)]
+
+
+@pytest.mark.parametrize("name,nn", GOLDEN_STDOUT)
+def test_host_stencil_stdout_equals_reference_program(gpu, name, nn):
+    """With the stencil nest on the host, the B200 program prints exactly what the
+    reference's own ExternalEvaluator.run_for_output printed for the same program
+    (tests/golden/*.stdout, oracle/pin_reference.py): the literal fp32 sequential
+    gosa, byte for byte -- also when other nests run on the device."""
+    from conftest import GOLDEN
+    want = (GOLDEN / f"himeno_{name.lower()}_n{nn}.stdout").read_text()
+    with B200Evaluator(name, nn=nn, poison_device=True) as ev:
+        for g in ("0000000000000", "0000000000100", "1001000000000"):
+            genome = tuple(int(c) for c in g)
+            assert ev.run_for_output(genome, literal_gosa=False) == want, (name, nn, g)
+            assert ev.stats[genome]["gosa_f32_literal"], g
+        # stencil on the device (kernels / gang rows / the device time loop, fused and
+        # two-step): verification mode sums the pattern's own device terms in order
+        for g in ("0000000100100", "0000000001001", "0000001000000", "1001001000000",
+                  "0100100100100"):
+            genome = tuple(int(c) for c in g)
+            assert ev.run_for_output(genome) == want, (name, nn, g)
+            assert ev.stats[genome]["gosa_f32_literal"], g
+
+
+def test_device_stencil_gosa_f32_is_rounded_fp64(gpu):
+    with B200Evaluator("XS", nn=3) as ev:
+        for g in ("0000000100100", "0000001000000"):
+            genome = tuple(int(c) for c in g)
+            res = ev.run(genome)
+            assert not res.gosa_f32_literal
+            assert res.gosa_f32 == np.float32(res.gosa)
+
+
+def test_smem_optin_raised_on_every_device_used(gpu):
+    """The large-shared-memory kernels' opt-in is set per device context (a
+    process-wide flag would leave devices 1..7 without it)."""
+    with B200Evaluator("M", nn=4, devices="all") as ev:
+        ev.prepare()
+        for slot in range(ev.max_concurrency):
+            ev._context(slot)   # noqa: SLF001 - every device gets a context
+        for dev in sorted(set(ev.devices)):
+            # run the time-loop pattern on that device (two-step + single-step kernels)
+            ctx = ev._contexts[ev.devices.index(dev)]
+            ctx.init_device()
+            ctx.jacobi_device(3, 1)
+            ctx.sync()
+            assert N.smem_optin(7, dev) > 48 * 1024, dev   # two-step kernel, stash
+            assert N.smem_optin(1, dev) > 48 * 1024, dev   # single-step, 3 stages
+
+
+# --- BASELINE configs at full size ----------------------------------------------------------
+
+def test_headline_L_bench_step_matches_golden(gpu):
+    """The bench's step (L, jacobi(100), device time loop with two-step passes) against
+    the oracle's committed result (scripts/gen_golden_l100.py): p bit-exact (SHA-256 of
+    the field), gosa within 1e-11."""
+    import hashlib
+    import json
+    from conftest import GOLDEN
+    want = json.loads((GOLDEN / "himeno_l_n100.json").read_text())
+    sz = himeno.size("L")
+    with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+        ctx.init_device()
+        ctx.jacobi_device(want["nn"], 1)
+        p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+    assert hashlib.sha256(p.tobytes()).hexdigest() == want["p_sha256"]
+    assert abs(g - want["gosa64"]) <= 1e-11 * want["gosa64"]
+    for i, j, k, v in want["p_samples"]:
+        assert p[i, j, k] == np.float32(v)
+
+
+@pytest.fixture(scope="module")
+def xl_oracle():
+    """XL (config 5's grid) after 2 and after 4 iterations, threaded oracle."""
+    sz = himeno.size("XL")
+    f = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(f)
+    out = {}
+    g2, _ = oracle.jacobi(f, 2, threads=oracle.max_threads())
+    out[2] = (f["p"].copy(), g2)
+    g4, _ = oracle.jacobi(f, 2, threads=oracle.max_threads())   # iterations 3-4
+    out[4] = (f["p"], g4)
+    for name in list(f):
+        if name != "p":
+            del f[name]
+    return out
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+def test_xl_grid_bit_exact(gpu, xl_oracle, tb):
+    """XL 513x513x1025 (BASELINE config 5), one- and two-step kernels, nn = 2 and 4."""
+    sz = himeno.size("XL")
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            for nn in (2, 4):
+                ctx.init_device()
+                ctx.jacobi_device(nn, 1)
+                p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+                want_p, want_g = xl_oracle[nn]
+                assert np.array_equal(p, want_p), (tb, nn)
+                assert abs(g - want_g) <= 1e-11 * want_g, (tb, nn, g, want_g)
+                del p
+    finally:
+        lib.hp_set_temporal_blocking(old)
+
+
+@pytest.fixture(scope="module")
+def l_oracle_n4():
+    sz = himeno.size("L")
+    f = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(f)
+    g3, _ = oracle.jacobi(f, 3, threads=oracle.max_threads())
+    p3 = f["p"].copy()
+    g4, _ = oracle.jacobi(f, 1, threads=oracle.max_threads())
+    return {3: (p3, g3), 4: (f["p"].copy(), g4)}
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_l_grid_slabs_bit_exact(gpu, l_oracle_n4, ranks, tb):
+    """BASELINE config 3's decomposition (L split into 2/4/8 slabs, halo exchange and
+    gosa sum after the passes) with virtual ranks on one GPU, against the full grid."""
+    from paper_2002_12115_b200 import dd
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(tb)
+    try:
+        for nn in (3, 4):
+            with dd.GroupJacobi("L", [0] * ranks) as g:
+                gosa = g.jacobi(nn)
+                p = g.gather("p")
+            want_p, want_g = l_oracle_n4[nn]
+            assert np.array_equal(p, want_p), (ranks, tb, nn)
+            assert abs(gosa - want_g) <= 1e-11 * want_g, (ranks, tb, nn)
+    finally:
+        lib.hp_set_temporal_blocking(old)

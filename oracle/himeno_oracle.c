@@ -176,6 +176,49 @@ int oracle_initmt(int I, int J, int K, float* const* fields) {
   return 0;
 }
 
+/* initmt with the planes first touched by the OpenMP threads that compute them
+ * in oracle_jacobi (same static schedule over i): the arrays' pages land on the
+ * NUMA node of their thread (for the multi-threaded CPU baseline).  Same values
+ * as initmt. */
+int oracle_initmt_par(int I, int J, int K, float* const* fields, int threads) {
+  if (I < 4 || J < 4 || K < 4 || !fields) return -1;
+  fields_t F;
+  F.I = I; F.J = J; F.K = K;
+  for (int f = 0; f < NF; f++) F.f[f] = fields[f];
+  if (threads <= 1) {
+    initmt(&F);
+    return 0;
+  }
+#ifdef _OPENMP
+  const int imax = I - 1, jmax = J - 1, kmax = K - 1;
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (int i = 0; i < I; i++) {
+    for (int j = 0; j < J; j++)
+      for (int k = 0; k < K; k++) {
+        size_t c = at(&F, i, j, k);
+        for (int f = 0; f < NF; f++) F.f[f][c] = 0.0f;   /* wrk2 too: first touch */
+      }
+    if (i < imax)
+      for (int j = 0; j < jmax; j++)
+        for (int k = 0; k < kmax; k++) {
+          size_t c = at(&F, i, j, k);
+          F.f[F_A0][c] = 1.0f;
+          F.f[F_A1][c] = 1.0f;
+          F.f[F_A2][c] = 1.0f;
+          F.f[F_A3][c] = (float)(1.0 / 6.0);
+          F.f[F_C0][c] = 1.0f;
+          F.f[F_C1][c] = 1.0f;
+          F.f[F_C2][c] = 1.0f;
+          F.f[F_P][c] = (float)(i * i) / (float)((imax - 1) * (imax - 1));
+          F.f[F_BND][c] = 1.0f;
+        }
+  }
+#else
+  initmt(&F);
+#endif
+  return 0;
+}
+
 /* jacobi(nn) only, on the given state; threads > 1 uses OpenMP over i planes
  * (fp64 gosa only; p/wrk2 identical to the sequential run). */
 int oracle_jacobi(int I, int J, int K, int nn, float* const* fields, int threads,

@@ -40,6 +40,7 @@ def lib():
         l.oracle_initmt.argtypes = [C.c_int, C.c_int, C.c_int, P]
         l.oracle_jacobi.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int,
                                     C.POINTER(C.c_double), C.POINTER(C.c_float)]
+        l.oracle_initmt_par.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_int]
         l.oracle_max_threads.restype = C.c_int
         _lib = l
     return _lib
@@ -73,6 +74,13 @@ def initmt(fields: dict) -> None:
     I, J, K = fields["p"].shape
     if lib().oracle_initmt(I, J, K, _ptrs(fields)) != 0:
         raise ValueError("oracle_initmt: bad arguments")
+
+
+def initmt_parallel(fields: dict, threads: int) -> None:
+    """initmt with NUMA-friendly first touch (planes by the threads that compute them)."""
+    I, J, K = fields["p"].shape
+    if lib().oracle_initmt_par(I, J, K, _ptrs(fields), threads) != 0:
+        raise ValueError("oracle_initmt_par: bad arguments")
 
 
 def jacobi(fields: dict, nn: int, threads: int = 1) -> tuple:

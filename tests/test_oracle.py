@@ -60,3 +60,21 @@ def test_zero_iterations_leave_initial_state():
     i = 3
     assert p[i, 1, 1] == np.float32(i * i) / np.float32((imax - 1) * (imax - 1))
     assert res["gosa64"] == 0.0
+
+
+def test_parallel_first_touch_initmt_is_initmt():
+    sz = himeno.custom_size(21, 17, 40)
+    a = oracle.empty_fields(sz.I, sz.J, sz.K)
+    b = oracle.empty_fields(sz.I, sz.J, sz.K)
+    oracle.initmt(a)
+    oracle.initmt_parallel(b, 4)
+    for name in oracle.FIELDS:
+        assert np.array_equal(a[name], b[name]), name
+
+
+def test_cpu_bench_subprocess_reports_its_procedure():
+    """bench.py's two CPU legs share this procedure (fresh process, bound threads)."""
+    from oracle import cpu_bench
+    r = cpu_bench.run_subprocess("XS", 0.2, 2, min_iters=3)
+    assert r["value"] > 0 and r["cores"] == 2 and r["iterations"] >= 3
+    assert r["omp"]["OMP_PROC_BIND"] and "first touch" in r["sample"]

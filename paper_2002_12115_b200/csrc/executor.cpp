@@ -38,9 +38,32 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "context.h"
 
 using namespace hp;
+
+// NVTX ranges (header-only NVTX3: a no-op unless a profiler is attached): one per
+// program run, per loop execution (device launch / host nest, by loop id) and per
+// transfer, so an nsys/ncu timeline reads in the program's own terms.
+namespace {
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+const char* loop_range_name(int loop, bool device) {
+  static const char* const dev[HP_NLOOPS] = {
+      "loop 0 device", "loop 1 device", "loop 2 device", "loop 3 device", "loop 4 device",
+      "loop 5 device", "loop 6 device", "loop 7 device", "loop 8 device", "loop 9 device",
+      "loop 10 device", "loop 11 device", "loop 12 device"};
+  static const char* const host[HP_NLOOPS] = {
+      "loop 0 host", "loop 1 host", "loop 2 host", "loop 3 host", "loop 4 host",
+      "loop 5 host", "loop 6 host", "loop 7 host", "loop 8 host", "loop 9 host",
+      "loop 10 host", "loop 11 host", "loop 12 host"};
+  return loop >= 0 && loop < HP_NLOOPS ? (device ? dev[loop] : host[loop]) : "loop";
+}
+}  // namespace
 
 // ------------------------------------------------------------------ errors
 
@@ -516,6 +539,7 @@ struct Runner {
   // copy is entirely stale -- SURVEY.md B.2); without it the whole array is.
   void h2d(int v, bool implicit) {
     if (failed()) return;
+    Nvtx range(implicit ? "h2d (implicit)" : "h2d");
     const VarInfo& vi = kVars[v];
     if (vi.nfields) {
       const std::vector<Box> boxes = guard ? C->coh[v].region_excluding(OWN_DEV, full_box())
@@ -562,6 +586,7 @@ struct Runner {
   // the host; without it the whole array is copied, as a literal `update self`.
   void d2h(int v, bool implicit) {
     if (failed()) return;
+    Nvtx range(implicit ? "d2h (implicit)" : "d2h");
     const VarInfo& vi = kVars[v];
     const double t0 = now_s();
     if (vi.nfields) {
@@ -770,6 +795,7 @@ struct Runner {
     const int loop = kNestLoops[nest][level];
     fire_all(before[loop]);
     if (on_device(loop)) {
+      Nvtx range(loop_range_name(loop, true));
       launch(nest, mapping(loop), b, level == 0);
     } else if (level < 2 && busy_below[loop]) {
       const int lo = level == 0 ? b.i0 : b.j0, hi = level == 0 ? b.i1 : b.j1;
@@ -781,6 +807,7 @@ struct Runner {
         if (level == 0) check_time();
       }
     } else {
+      Nvtx range(loop_range_name(loop, false));
       host_nest(nest, b);
       check_time();
     }
@@ -792,6 +819,7 @@ struct Runner {
   // device-resident time loop (gene 6 = 1)
   void device_time_loop() {
     if (failed()) return;
+    Nvtx range(loop_range_name(6, true));
     // implicit copies for everything the loop body touches
     std::vector<int> imp, tmp;
     implicit_vars(NEST_STENCIL, tmp);
@@ -1090,7 +1118,10 @@ extern "C" int hp_run(hp_ctx* c, const hp_schedule* s, hp_result* r) {
 
   run.t_start = now_s();
   run.deadline = s->timeout_s > 0 ? run.t_start + s->timeout_s : 0;
-  run.program();
+  {
+    Nvtx range("hp_run program");
+    run.program();
+  }
   if (run.status == HP_TIMEOUT || run.status == HP_FAIL_LAUNCH) cudaStreamSynchronize(c->stream);
   r->wall_s = now_s() - run.t_start;
   run.finish_literal();   // verification mode only; not part of the timed run

@@ -255,9 +255,18 @@ int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
 
 /* Diagnostics: the dynamic shared-memory limit (bytes) the large-shared-memory
  * kernel `id` has in `device`'s context (0..2 single-step stencil with 2..4
- * stages, 3..6 two-step shapes, 7 two-step with the tensor-memory stash).  The
- * library raises it per device before the first launch there. */
+ * stages, 3..6 two-step shapes, 7 two-step with the tensor-memory stash, 8 the
+ * two-step tile-exchange kernel).  The library raises it per device before the
+ * first launch there. */
 int hp_smem_optin(int id, int device, int* bytes);
+/* Diagnostics: the kernel the most recent two-step pass (any context) launched:
+ * 0 none yet, 1 k_stencil_tb2 (halo-recomputing tiles), 2 k_stencil_tx (tiles
+ * exchanging their p1 boundary through L2). */
+int hp_last_two_step_kernel(void);
+/* Diagnostics: 1 if an exchange-kernel launch of this context ever timed out
+ * waiting for a neighbour tile (its results are invalid and gosa was set to NaN),
+ * 0 if not, <0 on error.  Synchronous. */
+int hp_tx_status(hp_ctx* ctx);
 
 /* Pinned host buffers for callers without their own allocator (e2e inputs). */
 void* hp_host_alloc(size_t bytes);

@@ -53,7 +53,8 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     newest = max(p.stat().st_mtime for p in
-                 _sources() + sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h")) + [Path(__file__)])
+                 _sources() + sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) +
+                 sorted(INCLUDE.glob("*.h")) + [Path(__file__)])
     return newest > LIB.stat().st_mtime
 
 

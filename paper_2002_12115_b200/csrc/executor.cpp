@@ -220,7 +220,10 @@ extern "C" void hp_destroy(hp_ctx* c) {
   for (float* h : c->host)
     if (h) cudaFreeHost(h);
   if (c->hscal) cudaFreeHost(c->hscal);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream) {
+    tx_forget_stream(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
   delete c;
 }
 
@@ -1233,6 +1236,13 @@ extern "C" int hp_jacobi_device(hp_ctx* c, int nn, int variant) {
 extern "C" uint64_t hp_launch_count(hp_ctx* c) { return c ? c->launches : 0; }
 
 extern "C" int hp_set_temporal_blocking(int on) { return set_temporal_blocking(on); }
+
+extern "C" int hp_tx_status(hp_ctx* c) {
+  if (!c) return HP_ERR_ARG;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int r = tx_error(c->dev.tma);
+  return r < 0 ? cuda_fail(cudaGetLastError(), "hp_tx_status") : r;
+}
 
 extern "C" int hp_set_stencil_config(int cfg) {
   const int n = set_stencil_config(cfg);

@@ -119,6 +119,12 @@ int set_temporal_blocking(int on);
 // raise a kernel's dynamic shared-memory limit on the current device (once per
 // kernel and device); false if the runtime refuses
 bool ensure_smem_optin(const void* func, int bytes);
+// exchange-kernel launches are chained per device across streams (stencil_tma.cu);
+// a stream about to be destroyed must be dropped from that chain
+void tx_forget_stream(cudaStream_t s);
+// 1 if an exchange launch of this context timed out waiting for a neighbour, 0 if
+// not, -1 on a CUDA error (synchronous read)
+int tx_error(const void* tma);
 const void* smem_kernel(int id);   // the opted-in kernels by id (hp_smem_optin)
 void set_error(const char* fmt, ...);   // executor.cpp: hp_last_error() text
 int cuda_fail(cudaError_t e, const char* what);

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -944,15 +945,28 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   gosa_commit_units(g, units.count, reset);
 }
 
+#include "stencil_tx.cuh"
+
 // ------------------------------------------------------------------ host side
+
+constexpr int kTxTJ = 7;   // rows per exchange tile (L: 4 x 37 tiles = 148 SMs)
 
 struct TmaState {
   StencilMaps base;          // coefficient maps + p map
   CUtensorMap scratch_map;   // p map of the rotation buffer
   Tb2Maps tb2[kTb2Shapes];   // two-step kernel shapes: coefficient boxes + p map
   CUtensorMap tb2_scratch[kTb2Shapes];
+  TxMaps tx;                 // exchange kernel: coefficient boxes 128 x TJ + p map
+  CUtensorMap tx_scratch;
   const float* p;
   const float* scratch;
+  // exchange buffers (k_stencil_tx), sized for this context's j/k extents
+  uint2* xr = nullptr;       // tagged boundary words {value, tag}
+  uint2* xc = nullptr;
+  size_t nxr = 0, nxc = 0;   // words
+  unsigned* err = nullptr;
+  int tx_ktiles = 0, tx_jtiles = 0, tx_chunks = 0;   // capacity (0: exchange kernel off)
+  unsigned epoch = 0;
 };
 
 }  // namespace
@@ -995,16 +1009,60 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   encode_tb2(t->tb2[1], t->tb2_scratch[1], Tb2<16, 8, 4>::QK, Tb2<16, 8, 4>::R1);
   encode_tb2(t->tb2[2], t->tb2_scratch[2], Tb2<16, 6, 5>::QK, Tb2<16, 6, 5>::R1);
   encode_tb2(t->tb2[3], t->tb2_scratch[3], Tb2<16, 5, 6>::QK, Tb2<16, 5, 6>::R1);
+  {
+    static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
+                                      HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
+    for (int m = 0; m < NCOEF; ++m)
+      ok = ok && encode(&t->tx.coef[m], F, F.f[fields[m]], XK, kTxTJ, pc[2], dk);
+    ok = ok && encode(&t->tx.pin, F, F.f[HP_F_P], XW, kTxTJ + 2, pc[3], dk);
+    ok = ok && encode(&t->tx_scratch, F, scratch, XW, kTxTJ + 2, pc[3], dk);
+  }
   t->p = F.f[HP_F_P];
   t->scratch = scratch;
   if (!ok) {
     delete t;
     return nullptr;
   }
+  // exchange buffers for the j/k extents of this context (slab contexts share the
+  // global j/k extents): tiles of 128 k x TJ j over [0, K-2) x [1, J-2), only when
+  // every tile can be resident at once
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ktiles = (F.K - 2 + XK - 1) / XK;
+    const int jtiles = (F.J - 3 + kTxTJ - 1) / kTxTJ;
+    const int tiles = ktiles * jtiles;
+    if (tiles >= 1 && sms > 0 && tiles <= sms && F.K >= 4 && F.J >= 4) {
+      const int chunks = sms / tiles;
+      const size_t xrw = (size_t)XK * ktiles + 8, xcw = ((size_t)kTxTJ * jtiles + 8) * XCP;
+      const size_t nxr = (size_t)XRX * chunks * jtiles * 2 * xrw;
+      const size_t nxc = (size_t)XRX * chunks * ktiles * 2 * xcw;
+      // zeroed: tags start at epoch 1 (4097), so no stale word can match
+      if (cudaMalloc(&t->xr, nxr * 8) == cudaSuccess && cudaMalloc(&t->xc, nxc * 8) == cudaSuccess &&
+          cudaMalloc(&t->err, 4) == cudaSuccess && cudaMemset(t->xr, 0, nxr * 8) == cudaSuccess &&
+          cudaMemset(t->xc, 0, nxc * 8) == cudaSuccess && cudaMemset(t->err, 0, 4) == cudaSuccess) {
+        t->nxr = nxr;
+        t->nxc = nxc;
+        t->tx_ktiles = ktiles;
+        t->tx_jtiles = jtiles;
+        t->tx_chunks = chunks;
+      } else {
+        cudaGetLastError();   // no exchange kernel for this context (tb2 runs instead)
+      }
+    }
+  }
   return t;
 }
 
-void destroy_stencil_tma(void* h) { delete static_cast<TmaState*>(h); }
+void destroy_stencil_tma(void* h) {
+  TmaState* t = static_cast<TmaState*>(h);
+  if (!t) return;
+  if (t->xr) cudaFree(t->xr);
+  if (t->xc) cudaFree(t->xc);
+  if (t->err) cudaFree(t->err);
+  delete t;
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) changes the kernel in the
 // *current device's* context only, so the opt-in is recorded per (kernel, device):
@@ -1039,6 +1097,7 @@ const void* smem_kernel(int id) {
     case 5: return (const void*)k_stencil_tb2<16, 6, 5, false>;
     case 6: return (const void*)k_stencil_tb2<16, 5, 6, false>;
     case 7: return (const void*)k_stencil_tb2<16, 8, 4, true>;
+    case 8: return (const void*)k_stencil_tx<kTxTJ>;
     default: return nullptr;
   }
 }
@@ -1221,6 +1280,128 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   return e == cudaSuccess ? 1 : -1;
 }
 
+// ---- exchange kernel launches --------------------------------------------------
+// Its CTAs wait on each other, so two exchange launches must never share a device
+// at the same time (each could hold part of the SMs the other needs).  Launches
+// of different streams on one device are therefore chained in enqueue order: a
+// launch on stream s first waits for everything the previously used stream had
+// enqueued (an event recorded there).  Consecutive launches on one stream need
+// nothing (stream order; PDL keeps overlapping their tails).  Any other kernel
+// that overlaps an exchange launch finishes on its own, so the launch's CTAs all
+// become resident eventually.
+static std::mutex g_tx_mu;
+struct TxLane {
+  cudaStream_t last = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+static std::map<int, TxLane> g_tx_lanes;
+
+void tx_forget_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_tx_mu);
+  for (auto& kv : g_tx_lanes)
+    if (kv.second.last == s) kv.second.last = nullptr;   // stream is being destroyed
+}
+
+// HIMENO_TX: 0 (default) = never, 1 = when tiles x chunks fill at least half the
+// SMs, 2 = whenever the tiles fit (tests: small and ragged grids).  Off by default:
+// on L it reads 7% fewer DRAM bytes than k_stencil_tb2 but runs 4% slower
+// (profiles/r02_tx_experiments.md).  Read per launch so tests can switch it.
+static int tx_mode() {
+  const int v = env_int("HIMENO_TX");
+  return v < 0 ? 0 : v;
+}
+// planes per chunk at least this many (HIMENO_TX_MINCHUNK; a chunk recomputes two
+// planes at each end)
+static int tx_min_chunk() {
+  const int v = env_int("HIMENO_TX_MINCHUNK");
+  return v > 0 ? v : 16;
+}
+
+static int launch_tx(TmaState* t, const DevFields& F, const float* p_in, float* p_out, int i_lo,
+                     int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi,
+                     const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+  constexpr int TJ = kTxTJ;
+  using T = Tx<TJ>;
+  const int mode = tx_mode();
+  // a pinned two-step shape (sweeps, tests) asks for k_stencil_tb2
+  if (mode == 0 || !t->xr || env_int("HIMENO_TB2_SHAPE") >= 0) return 0;
+  const int ktiles = (k_hi + XK - 1) / XK;
+  const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
+  const int tiles = ktiles * jtiles;
+  if (ktiles > t->tx_ktiles || jtiles > t->tx_jtiles || tiles > sms) return 0;
+  const int ni = i_hi - i_lo;
+  int chunks = std::min(t->tx_chunks, sms / tiles);
+  chunks = std::max(1, std::min(chunks, ni / tx_min_chunk()));
+  const int chunk = (ni + chunks - 1) / chunks;
+  chunks = (ni + chunk - 1) / chunk;
+  if (chunk + 2 >= (int)kXEpoch) return 0;
+  if (mode == 1 && tiles * chunks * 2 < sms) return 0;
+  if (tiles * chunks > g.capacity) return 0;
+  const size_t smem = T::smem_bytes();
+  if (!ensure_smem_optin((const void*)k_stencil_tx<TJ>, (int)smem)) return -1;
+  TxMaps maps = t->tx;
+  if (p_in == t->scratch) maps.pin = t->tx_scratch;
+  XBuf x;
+  x.xr = t->xr;
+  x.xc = t->xc;
+  x.err = t->err;
+  x.xrw = XK * ktiles + 8;
+  x.xcw = (TJ * jtiles + 8) * XCP;
+  x.chunks = chunks;
+  x.dbg = std::max(0, env_int("HIMENO_TX_DBG"));
+  x.ahead = env_int("HIMENO_TX_AHEAD") > 0 ? std::min(env_int("HIMENO_TX_AHEAD"), XNS - 2) : XNS - 2;
+  x.xrx = XRX;
+  if (env_int("HIMENO_TX_XRX") > 0) x.xrx = std::min(XRX, env_int("HIMENO_TX_XRX"));
+  if (x.xrx < 10 + 2 * x.ahead || (x.xrx & (x.xrx - 1))) x.xrx = XRX;
+  x.evl = env_int("HIMENO_TX_EVL") != 0 ? 1 : 0;   // evict_last: default (10% faster)
+  std::lock_guard<std::mutex> lock(g_tx_mu);
+  if (++t->epoch >= (1u << 20)) {   // tags epoch * 4096 + plane stay in 32 bits
+    if (cudaMemsetAsync(t->xr, 0, t->nxr * 8, s) != cudaSuccess ||
+        cudaMemsetAsync(t->xc, 0, t->nxc * 8, s) != cudaSuccess)
+      return -1;
+    t->epoch = 1;
+  }
+  x.epoch = t->epoch;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TxLane& lane = g_tx_lanes[dev];
+  if (lane.last && lane.last != s) {
+    if (!lane.ev && cudaEventCreateWithFlags(&lane.ev, cudaEventDisableTiming) != cudaSuccess)
+      return -1;
+    if (cudaEventRecord(lane.ev, lane.last) != cudaSuccess ||
+        cudaStreamWaitEvent(s, lane.ev, 0) != cudaSuccess)
+      return -1;
+  }
+  lane.last = s;
+  static const bool pdl = env_int("HIMENO_TB2_PDL") != 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)(tiles * chunks));
+  cfg.blockDim = dim3(T::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const cudaError_t e =
+      cudaLaunchKernelEx(&cfg, k_stencil_tx<TJ>, maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                         ktiles, jtiles, chunk, g_lo, g_hi, a.omega, g, a.gosa_reset, x);
+  return e == cudaSuccess ? 1 : -1;
+}
+
+// which two-step kernel the last two-step pass launched: 1 = k_stencil_tb2,
+// 2 = k_stencil_tx (hp_last_two_step_kernel; tests and bench.py name it)
+static std::atomic<int> g_last_two_step{0};
+
+int tx_error(const void* h) {
+  const TmaState* t = static_cast<const TmaState*>(h);
+  if (!t || !t->err) return 0;
+  unsigned v = 0;
+  if (cudaMemcpy(&v, t->err, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return v ? 1 : 0;
+}
+
 // Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not
 // applicable: caller runs two single steps), or -1 on launch error.
 int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
@@ -1235,6 +1416,16 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (!full && (i_lo < 2 || i_hi > F.I - 2)) return 0;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   const int g_lo = 1 - a.i_off, g_hi = a.imax - 1 - a.i_off;
+  // the exchange kernel when this geometry's tiles can all be resident
+  {
+    const int r = launch_tx(const_cast<TmaState*>(t), F, p_in, p_out, i_lo, i_hi, j_lo, j_hi,
+                            k_lo, k_hi, g_lo, g_hi, a, g, s, sms);
+    if (r != 0) {
+      g_last_two_step = 2;
+      return r;
+    }
+  }
+  g_last_two_step = 1;
   const Tb2Choice c = tb2_choose(i_hi - i_lo, j_hi - j_lo, k_hi, sms);
   const int v = c.shape;
   Tb2Maps maps = t->tb2[v];
@@ -1256,6 +1447,8 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
 }
 
 }  // namespace hp
+
+extern "C" int hp_last_two_step_kernel(void) { return hp::g_last_two_step.load(); }
 
 // Diagnostics: the dynamic shared-memory limit kernel `id` has on `device`
 // (cudaFuncGetAttributes in that device's context).

@@ -1,0 +1,539 @@
+// k_stencil_tx<TJ>: two Jacobi iterations per pass with NO halo recomputation.
+// Included by stencil_tma.cu inside namespace hp { namespace { ... } } after the
+// two-step kernel (shares Row / load_row0 / ss_quad2 / the TMEM stash helpers).
+//
+// The two-step kernel k_stencil_tb2 makes every tile self-sufficient: step 1
+// recomputes p1 on a one-point halo around the step-2 outputs, so each tile
+// reads its coefficients on a 64 x 16 window for 56 x 14 outputs (1.31x the
+// bytes from L2, 1.31x the step-1 work), and the 190 tiles of the L grid do not
+// divide the 148 SMs.  Here the tiles partition the plane exactly -- 128 k x TJ j
+// points per tile, one tile column (a run of planes) per CTA, every CTA resident
+// at once -- and neighbouring tiles swap their p1 boundary instead:
+//
+//   step-1 warps (TJ, warp r = row j0+r): p1 of the tile's own points only
+//       (coefficient box 128 x TJ: each coefficient is read from L2 once per pass);
+//       the first / last row and the first / last column of p1 are also stored,
+//       straight from registers, to a global exchange ring (L2) as tagged words
+//       {value, plane tag}: 64-bit, single-copy atomic, so no flag and no fence;
+//   exchange warp: for plane m, reads the (up to 8) neighbours' boundary words
+//       for its halo (two planes in flight), retries until every tag says plane
+//       m of this launch, and writes the values into the halo of the p1 slot;
+//   step-2 warps (TJ): p2 = S(p1) one plane behind, coefficients of plane m-1
+//       stashed in tensor memory (as in k_stencil_tb2), 128 x TJ outputs.
+//   producer warp: TMA of p0 planes (136 x TJ+2 box) and coefficient tiles.
+//
+// Halo cells that no tile owns (domain boundary, k = -1, rows past the tile
+// grid) are p0 = p1 (boundaries never change) and are written by the step-1
+// warps from their p0 rows; cells owned by a neighbour tile come from the
+// exchange.  The two sets are disjoint, so every halo cell has one writer.
+//
+// Planes: a CTA runs planes [ia, ib) of one tile (ia..ib = the whole interior on
+// L; on smaller grids the planes are split into chunks so that tiles x chunks
+// fill the SMs; a chunk boundary costs two recomputed planes, as in tb2).  The
+// exchange is between CTAs of the same chunk only.
+//
+// Co-residency: a CTA waits on its neighbours, so all CTAs of a launch must be
+// resident together: grid <= SMs, one CTA per SM (217 KB of shared memory), and
+// exchange launches on one device are serialised across contexts (tx_order).
+// A neighbour wait that exceeds 2 s (never expected) records an error instead of
+// hanging: gosa becomes NaN and hp_tx_status reports it.
+//
+// Arithmetic per element is the same as k_stencil_tb2 (bit-identical p).
+
+constexpr int XK = 128;        // owned columns per tile: 32 lanes x float4
+constexpr int XW = XK + 8;     // tile row stride: column c <-> k = k0 - 4 + c
+constexpr int XSP = 3;         // p0 ring slots
+constexpr int XSC = 4;         // coefficient stages
+constexpr int XSQ = 6;         // p1 ring slots
+constexpr int XNS = 5;         // TMEM stash slots per step-2 warp (48 columns each)
+// Global exchange ring depth.  A tile writes plane q's words only after its own
+// gather of plane q-8 (its coefficient stage q waits for the step-2 stash of plane
+// q-XSC = q-4, which may run XNS-2 = 3 planes ahead of the p1 plane step 2 waits
+// for, so after the gather of q-8), which needed every neighbour's words of q-8,
+// written after the neighbour's gather of q-16: so when slot q % XRX is rewritten
+// every reader has finished with plane q - XRX if XRX >= 16.
+constexpr int XRX = 32;
+// Column words are written by a different warp per row; packed, seven rows share two
+// 32-byte sectors and the partial-sector writes from several warps cost 6-19 us per
+// L pass (profiles/r02_tx_experiments.md); one word per sector does not.
+constexpr int XCP = 4;
+constexpr unsigned kXEpoch = 4096u;   // tag = epoch * kXEpoch + plane index + 1
+
+template <int TJ_>
+struct Tx {
+  static constexpr int TJ = TJ_;
+  static constexpr int kWarps = 2 * TJ + 2;
+  static constexpr int kThreads = kWarps * 32;
+  static constexpr uint32_t kTileBytes = XW * (TJ + 2) * 4;   // p0 tile == p1 slot
+  static constexpr uint32_t kTileSlot = (kTileBytes + 127) / 128 * 128;
+  static constexpr uint32_t kCExt = XK * TJ * 4;              // one coefficient array
+  static constexpr uint32_t kCSlot = NCOEF * kCExt;
+  static constexpr uint32_t kSmem = XSP * kTileSlot + XSC * kCSlot + XSQ * kTileSlot;
+  static constexpr int kBars = 2 * XSP + 2 * XSC + 2 * XSQ;
+  static constexpr size_t smem_bytes() { return 128 + (size_t)kSmem + kBars * sizeof(uint64_t); }
+  static_assert(smem_bytes() + 1024 <= 232448, "rings exceed the 227 KB of shared memory");
+};
+
+struct __align__(64) TxMaps {
+  CUtensorMap coef[NCOEF];   // box 128 x TJ, origin (k0, j0)
+  CUtensorMap pin;           // box 136 x (TJ+2), origin (k0-4, j0-1)
+};
+
+// exchange buffers of one launch (per context, allocated with the tensor maps);
+// words are {float bits, tag}
+struct XBuf {
+  uint2* xr;          // [XRX][chunks][jtiles][2][xrw]: first / last owned p1 row, at k + 4
+  uint2* xc;          // [XRX][chunks][ktiles][2][xcw]: first / last owned p1 column, at
+                      // (j - j_lo) * XCP: one word per 32-byte sector (see XCP)
+  unsigned* err;      // nonzero: a neighbour wait timed out
+  unsigned epoch;
+  int xrw, xcw, chunks;
+  int ahead;          // stash up to this many planes ahead (1 .. XNS - 2)
+  int xrx;            // ring depth in planes (power of two, <= XRX, >= 10 + 2 * ahead)
+  int evl;            // 1: exchange words stored with an L2 evict_last policy
+  int dbg;            // HIMENO_TX_DBG (experiments only): 1 = do not wait for the tags,
+                      // 2 = do not publish, 4 = rows not published, 8 = columns not
+                      // published (results are wrong with any of them)
+};
+
+// relaxed gpu-scope accesses of tagged words (L2, never a stale L1 line)
+__device__ __forceinline__ uint2 ld_word(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 ld_words2(const uint2* p) {   // two words, 16-byte aligned
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_word(uint2* p, float v, unsigned tag, uint64_t pol) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p),
+               "r"(__float_as_uint(v)), "r"(tag), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_words2(uint2* p, float a, float b, unsigned tag, uint64_t pol) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+               "r"(__float_as_uint(a)), "r"(tag), "r"(__float_as_uint(b)), "r"(tag), "l"(pol)
+               : "memory");
+}
+// L2 policy of the exchange words: evict_last keeps the ring resident (it is
+// rewritten every XRX planes; evicted dirty lines would cost DRAM writes)
+__device__ __forceinline__ uint64_t xpolicy(int evl) {
+  uint64_t pol;
+  if (evl)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// One plane's halo as this lane of the exchange warp loads it.
+struct Halo {
+  uint4 top[2], bot[2];        // rows j0-1 / j0+TJ, columns k0+4*lane .. +3
+  uint2 top_e, bot_e;          // lane 0: column k0-1, lane 31: column k0+128
+  uint2 left, right;           // lane < TJ: row j0+lane, columns k0-1 / k0+128
+};
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int TJ>
+__global__ void __launch_bounds__(Tx<TJ>::kThreads, 1)
+k_stencil_tx(const __grid_constant__ TxMaps maps, DevFields F, float* __restrict__ out, int i_lo,
+             int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int ktiles, int jtiles, int chunk,
+             int g_lo, int g_hi, float omega, GosaSink g, int reset, XBuf x) {
+  using T = Tx<TJ>;
+  constexpr int PW = XW;
+  constexpr int WP = 2 * TJ, WX = 2 * TJ + 1;   // producer, exchange
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  unsigned char* p0ring = smem;
+  unsigned char* cring = p0ring + XSP * T::kTileSlot;
+  unsigned char* p1ring = cring + XSC * T::kCSlot;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kSmem);
+  uint64_t* pfull = bars;
+  uint64_t* pempty = pfull + XSP;
+  uint64_t* cfull = pempty + XSP;
+  uint64_t* cempty = cfull + XSC;
+  uint64_t* qfull = cempty + XSC;     // step-1 threads + the exchange warp
+  uint64_t* qempty = qfull + XSQ;     // step-2 threads
+  __shared__ double unit_part[TJ];
+  __shared__ uint32_t tmem_base_s;
+  constexpr uint32_t kStashCols = 512;   // 2 step-2 warps per lane quarter x XNS x 48
+  static_assert(TJ <= 8, "stash: (warp % 4, block) per step-2 warp");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = ktiles * jtiles;
+  const int u = blockIdx.x;
+  const int t = u % tiles, ch = u / tiles;
+  const int kt = t % ktiles, jt = t / ktiles;
+  const int k0 = kt * XK, j0 = j_lo + jt * TJ;
+  const int ia = i_lo + ch * chunk, ib = min(i_hi, ia + chunk);
+  const int np = ib - ia + 2;   // step-1 planes ia-1 .. ib
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < XSP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], TJ); }
+    for (int s = 0; s < XSC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], 2 * TJ); }
+    for (int s = 0; s < XSQ; ++s) {
+      mbar_init(&qfull[s], TJ * 32 + 32);
+      mbar_init(&qempty[s], TJ * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == TJ) tmem_alloc(&tmem_base_s, kStashCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double acc = 0.0;
+  if (warp == WP) {
+    // ------------------------------------------------------------- producer
+    if (lane == 0) {
+      uint32_t sp = 0, sc = 0;
+      auto load_p0 = [&](int plane) {
+        const int slot = sp % XSP;
+        if (sp >= (uint32_t)XSP) mbar_wait(&pempty[slot], ((sp / XSP) - 1) & 1);
+        mbar_expect_tx(&pfull[slot], T::kTileBytes);
+        tma_load_3d(p0ring + slot * T::kTileSlot, &maps.pin, &pfull[slot], k0 - 4, j0 - 1, plane);
+        ++sp;
+      };
+      load_p0(ia - 2);
+      load_p0(ia - 1);
+      for (int m = ia - 1; m <= ib; ++m) {
+        load_p0(m + 1);
+        const int slot = sc % XSC;
+        if (sc >= (uint32_t)XSC) mbar_wait(&cempty[slot], ((sc / XSC) - 1) & 1);
+        mbar_expect_tx(&cfull[slot], NCOEF * T::kCExt);
+        for (int c = 0; c < NCOEF; ++c)
+          tma_load_3d(cring + slot * T::kCSlot + c * T::kCExt, &maps.coef[c], &cfull[slot], k0,
+                      j0, m);
+        ++sc;
+      }
+    }
+  } else if (warp < TJ) {
+    // ---------------------------------------------- step-1 warps (row j0+r)
+    const int r = warp;
+    const int kq = k0 + lane * 4;
+    const bool row_in = j0 + r < j_hi;
+    bool in1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) in1[e] = row_in && kq + e >= k_lo && kq + e < k_hi;
+    const bool kfirst = kt == 0, klast = kt == ktiles - 1;
+    const uint64_t pol = xpolicy(x.evl);   // L2 policy of the exchange words
+    const bool jfirst = jt == 0, jlast = jt == jtiles - 1;
+    uint32_t sc = 0;
+    int pslot = 0;
+    uint32_t pphase = 0;
+    auto next_p = [&]() {
+      if (++pslot == XSP) {
+        pslot = 0;
+        pphase ^= 1u;
+      }
+    };
+    Row am, a0, ap, bm, b0, bp;
+    for (int w = 0; w < 2; ++w) {
+      mbar_wait(&pfull[pslot], pphase);
+      const float* pt = reinterpret_cast<const float*>(p0ring + pslot * T::kTileSlot);
+      const Row x0 = load_row0<32>(pt, r, lane), x1 = load_row0<32>(pt, r + 1, lane),
+                x2 = load_row0<32>(pt, r + 2, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[pslot]);
+      if (w == 0) { am = x0; a0 = x1; ap = x2; } else { bm = x0; b0 = x1; bp = x2; }
+      next_p();
+    }
+#pragma unroll 1
+    for (int q = 0; q < np; ++q) {
+      const int m = ia - 1 + q;
+      const int cur = pslot;
+      mbar_wait(&pfull[cur], pphase);
+      const float* pt = reinterpret_cast<const float*>(p0ring + cur * T::kTileSlot);
+      const Row cm = load_row0<32>(pt, r, lane), c0 = load_row0<32>(pt, r + 1, lane),
+                cp = load_row0<32>(pt, r + 2, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[cur]);
+      next_p();
+      const int cslot = sc % XSC;
+      mbar_wait(&cfull[cslot], (sc / XSC) & 1);
+      const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + r * XK + lane * 4;
+      const bool plane_in = m >= g_lo && m < g_hi;
+      float v[4];
+      if (plane_in && row_in) {
+        float ss[4];
+        ss_quad2<XK * TJ>(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = in1[e] ? fadd(el(b0.v, e), fmul(omega, ss[e])) : el(b0.v, e);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = el(b0.v, e);
+      }
+      // boundary of the tile -> global exchange ring (tagged words, fire and forget)
+      if (!(x.dbg & 2)) {
+        const unsigned tag = x.epoch * kXEpoch + (unsigned)q + 1u;
+        const size_t xs = (size_t)(q & (x.xrx - 1)) * x.chunks + ch;
+        uint2* row = x.xr + (xs * jtiles + jt) * 2 * x.xrw + k0 + 4 + lane * 4;
+        uint2* col = x.xc + (xs * ktiles + kt) * 2 * x.xcw + ((j0 - j_lo) + r) * XCP;
+        if (!(x.dbg & 4)) {
+          if (r == 0) {
+            st_words2(row, v[0], v[1], tag, pol);
+            st_words2(row + 2, v[2], v[3], tag, pol);
+          }
+          if (r == TJ - 1) {
+            st_words2(row + x.xrw, v[0], v[1], tag, pol);
+            st_words2(row + x.xrw + 2, v[2], v[3], tag, pol);
+          }
+        }
+        if (!(x.dbg & 8)) {
+          if (lane == 0) st_word(col, v[0], tag, pol);
+          if (lane == 31) st_word(col + x.xcw, v[3], tag, pol);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[cslot]);
+      ++sc;
+      // p1(m) -> ring slot, once the step-2 warps have released its previous plane
+      const int qslot = q % XSQ;
+      if (q >= XSQ) mbar_wait(&qempty[qslot], ((q / XSQ) - 1) & 1);
+      float* s = reinterpret_cast<float*>(p1ring + qslot * T::kTileSlot);
+      *reinterpret_cast<float4*>(s + (r + 1) * PW + 4 + lane * 4) = make_float4(v[0], v[1], v[2], v[3]);
+      // halo cells no tile owns: p1 = p0
+      if (kfirst && lane == 0) s[(r + 1) * PW + 3] = b0.left;
+      if (klast && lane == 31) s[(r + 1) * PW + 4 + XK] = b0.right;
+      if (r == 0) {
+        if (jfirst) {
+          *reinterpret_cast<float4*>(s + 4 + lane * 4) = bm.v;
+          if (lane == 0) s[3] = bm.left;
+          if (lane == 31) s[4 + XK] = bm.right;
+        } else {
+          if (kfirst && lane == 0) s[3] = bm.left;
+          if (klast && lane == 31) s[4 + XK] = bm.right;
+        }
+      }
+      if (r == TJ - 1) {
+        float* h = s + (TJ + 1) * PW;
+        if (jlast) {
+          *reinterpret_cast<float4*>(h + 4 + lane * 4) = bp.v;
+          if (lane == 0) h[3] = bp.left;
+          if (lane == 31) h[4 + XK] = bp.right;
+        } else {
+          if (kfirst && lane == 0) h[3] = bp.left;
+          if (klast && lane == 31) h[4 + XK] = bp.right;
+        }
+      }
+      mbar_arrive(&qfull[qslot]);
+      am = bm; a0 = b0; ap = bp;
+      bm = cm; b0 = c0; bp = cp;
+    }
+  } else if (warp < 2 * TJ) {
+    // ------------------- step-2 warps (output row j0+w2), coefficients in TMEM
+    const int w2 = warp - TJ;
+    const uint32_t tl = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((w2 >> 2) * XNS * 48);
+    const int j = j0 + w2;
+    const int kq = k0 + lane * 4;
+    const bool row_in = j < j_hi;
+    bool in2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) in2[e] = row_in && kq + e >= k_lo && kq + e < k_hi;
+    // Stage sq's coefficients for this thread's quad -> TMEM slot sq % XNS, and the
+    // stage is released at once.  Stages are stashed in order, up to XNS - 2 planes
+    // ahead of the p1 plane being waited for, while the warp would otherwise sit in
+    // that wait: the coefficient ring never waits for the exchange.
+    int st = 0;
+    auto stash = [&](int sq) {
+      const int cslot = sq % XSC;
+      const int ms = ia - 1 + sq;
+      if (ms >= ia && ms < ib) {   // planes that carry an output plane
+        const float* ct = reinterpret_cast<const float*>(cring + cslot * T::kCSlot) + w2 * XK + lane * 4;
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          float v[16];
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 qv = *reinterpret_cast<const float4*>(ct + (4 * kk + c4) * (XK * TJ));
+            v[4 * c4] = qv.x; v[4 * c4 + 1] = qv.y; v[4 * c4 + 2] = qv.z; v[4 * c4 + 3] = qv.w;
+          }
+          tmem_st16(tl + (uint32_t)((sq % XNS) * 48 + 16 * kk), v);
+        }
+        tmem_wait_st();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[cslot]);
+    };
+    Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
+#pragma unroll 1
+    for (int q = 0; q < np; ++q) {
+      const int m = ia - 1 + q;
+      while (st <= q) {
+        mbar_wait(&cfull[st % XSC], (st / XSC) & 1);
+        stash(st);
+        ++st;
+      }
+      const int qslot = q % XSQ;
+      // p1 plane q; meanwhile stash the stages that have landed
+#pragma unroll 1
+      while (!__any_sync(0xffffffffu, mbar_try(&qfull[qslot], (q / XSQ) & 1))) {
+        if (st < np && st <= q + x.ahead &&
+            __all_sync(0xffffffffu, mbar_test(&cfull[st % XSC], (st / XSC) & 1))) {
+          stash(st);
+          ++st;
+        }
+      }
+      mbar_wait(&qfull[qslot], (q / XSQ) & 1);   // complete: acquire for every lane
+      const float* s = reinterpret_cast<const float*>(p1ring + qslot * T::kTileSlot);
+      const Row nm = load_row0<32>(s, w2, lane), n0 = load_row0<32>(s, w2 + 1, lane),
+                npr = load_row0<32>(s, w2 + 2, lane);
+      mbar_arrive(&qempty[qslot]);
+      if (m >= ia + 1) {
+        float cv[48];
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)(((q - 1) % XNS) * 48 + 16 * kk), v);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) cv[16 * kk + e] = v[e];
+        }
+        tmem_wait_ld24(cv);
+        tmem_wait_ld24(cv + 24);
+        auto Q = [&](int c) {
+          return make_float4(cv[4 * c], cv[4 * c + 1], cv[4 * c + 2], cv[4 * c + 3]);
+        };
+        float ss[4];
+        ss_quad2q(Q, ym, y0, yp, zm, z0, zp, nm, n0, npr, ss);
+        float w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          w[e] = fadd(el(z0.v, e), fmul(omega, ss[e]));
+          if (in2[e]) acc += (double)fmul(ss[e], ss[e]);
+        }
+        if (row_in) {
+          float* o = out + F.at(m - 1, j, kq);
+          if (in2[0] && in2[1] && in2[2] && in2[3]) {
+            *reinterpret_cast<float4*>(o) = make_float4(w[0], w[1], w[2], w[3]);
+          } else {
+            for (int e = 0; e < 4; ++e)
+              if (in2[e]) o[e] = w[e];
+          }
+        }
+      }
+      ym = zm; y0 = z0; yp = zp;
+      zm = nm; z0 = n0; zp = npr;
+    }
+    unit_partial(g, (uint32_t)u, acc, unit_part, w2, TJ, 1);
+    acc = 0.0;
+  } else if (warp == WX) {
+    // --------------------------------------------------------- exchange warp
+    // Halo of plane q from the neighbours' boundary words; two planes in flight
+    // (the second's loads overlap the first's round trip).  A plane is committed
+    // once every word it needs carries its tag; otherwise it is reloaded.
+    const bool up = jt > 0, down = jt < jtiles - 1, lft = kt > 0, rgt = kt < ktiles - 1;
+    const int jy0 = j0 - j_lo;
+    auto load = [&](int q, Halo& h) {
+      const size_t xs = (size_t)(q & (x.xrx - 1)) * x.chunks + ch;
+      if (up) {   // last row of the tiles above
+        const uint2* src = x.xr + (xs * jtiles + (jt - 1)) * 2 * x.xrw + x.xrw + k0;
+        h.top[0] = ld_words2(src + 4 + lane * 4);
+        h.top[1] = ld_words2(src + 6 + lane * 4);
+        if (lane == 0 && lft) h.top_e = ld_word(src + 3);
+        if (lane == 31 && rgt) h.top_e = ld_word(src + 4 + XK);
+      }
+      if (down) {   // first row of the tiles below
+        const uint2* src = x.xr + (xs * jtiles + (jt + 1)) * 2 * x.xrw + k0;
+        h.bot[0] = ld_words2(src + 4 + lane * 4);
+        h.bot[1] = ld_words2(src + 6 + lane * 4);
+        if (lane == 0 && lft) h.bot_e = ld_word(src + 3);
+        if (lane == 31 && rgt) h.bot_e = ld_word(src + 4 + XK);
+      }
+      if (lane < TJ) {
+        if (lft) h.left = ld_word(x.xc + (xs * ktiles + (kt - 1)) * 2 * x.xcw + x.xcw + (jy0 + lane) * XCP);
+        if (rgt) h.right = ld_word(x.xc + (xs * ktiles + (kt + 1)) * 2 * x.xcw + (jy0 + lane) * XCP);
+      }
+    };
+    auto ready = [&](const Halo& h, unsigned tag) -> bool {
+      bool ok = true;
+      if (up) {
+        ok = ok && h.top[0].y == tag && h.top[0].w == tag && h.top[1].y == tag && h.top[1].w == tag;
+        if ((lane == 0 && lft) || (lane == 31 && rgt)) ok = ok && h.top_e.y == tag;
+      }
+      if (down) {
+        ok = ok && h.bot[0].y == tag && h.bot[0].w == tag && h.bot[1].y == tag && h.bot[1].w == tag;
+        if ((lane == 0 && lft) || (lane == 31 && rgt)) ok = ok && h.bot_e.y == tag;
+      }
+      if (lane < TJ) {
+        if (lft) ok = ok && h.left.y == tag;
+        if (rgt) ok = ok && h.right.y == tag;
+      }
+      return __all_sync(0xffffffffu, ok);
+    };
+    auto commit = [&](int q, const Halo& h) {
+      float* s = reinterpret_cast<float*>(p1ring + (q % XSQ) * T::kTileSlot);
+      if (up) {
+        *reinterpret_cast<float4*>(s + 4 + lane * 4) =
+            make_float4(__uint_as_float(h.top[0].x), __uint_as_float(h.top[0].z),
+                        __uint_as_float(h.top[1].x), __uint_as_float(h.top[1].z));
+        if (lane == 0 && lft) s[3] = __uint_as_float(h.top_e.x);
+        if (lane == 31 && rgt) s[4 + XK] = __uint_as_float(h.top_e.x);
+      }
+      if (down) {
+        float* d = s + (TJ + 1) * PW;
+        *reinterpret_cast<float4*>(d + 4 + lane * 4) =
+            make_float4(__uint_as_float(h.bot[0].x), __uint_as_float(h.bot[0].z),
+                        __uint_as_float(h.bot[1].x), __uint_as_float(h.bot[1].z));
+        if (lane == 0 && lft) d[3] = __uint_as_float(h.bot_e.x);
+        if (lane == 31 && rgt) d[4 + XK] = __uint_as_float(h.bot_e.x);
+      }
+      if (lane < TJ) {
+        if (lft) s[(lane + 1) * PW + 3] = __uint_as_float(h.left.x);
+        if (rgt) s[(lane + 1) * PW + 4 + XK] = __uint_as_float(h.right.x);
+      }
+      mbar_arrive(&qfull[q % XSQ]);
+    };
+    auto slot_free = [&](int q) {
+      return q < XSQ || __all_sync(0xffffffffu, mbar_test(&qempty[q % XSQ], ((q / XSQ) - 1) & 1));
+    };
+    Halo h0{}, h1{};
+    uint64_t t0 = 0;
+    int q = 0;
+#pragma unroll 1
+    while (q < np) {
+      // the slot: sleep in try_wait rather than spin (a spin takes issue slots from
+      // the stencil warps of this sub-partition: measured 5%)
+      if (q >= XSQ) mbar_wait(&qempty[q % XSQ], ((q / XSQ) - 1) & 1);
+      const bool two = q + 1 < np && slot_free(q + 1);
+      load(q, h0);
+      if (two) load(q + 1, h1);
+      const unsigned tag = x.epoch * kXEpoch + (unsigned)q + 1u;
+      if ((x.dbg & 1) || ready(h0, tag)) {
+        commit(q, h0);
+        ++q;
+        t0 = 0;
+        if (two && ((x.dbg & 1) || ready(h1, tag + 1u))) {
+          commit(q, h1);
+          ++q;
+        }
+      } else {
+        const uint64_t now = global_ns();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > 2000000000ull) {   // 2 s: never legitimate
+          if (lane == 0) atomicExch(x.err, 1u);
+          commit(q, h0);   // garbage halo, but the pipeline drains (gosa -> NaN)
+          ++q;
+          t0 = 0;
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == TJ) {
+    tmem_fence_after();
+    tmem_dealloc(tmem_base_s, kStashCols);
+  }
+  gosa_commit_units(g, gridDim.x, reset);
+  if (threadIdx.x == 0 && *(volatile unsigned*)x.err) *g.slot = __longlong_as_double(0x7ff8000000000000ll);
+}

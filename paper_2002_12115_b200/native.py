@@ -121,6 +121,8 @@ SIGNATURES = {
     "hp_dd_jacobi": (C.c_int, [_CtxP, C.c_int]),
     "hp_dd_time_steps": (C.c_int, [_CtxP, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "hp_smem_optin": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "hp_last_two_step_kernel": (C.c_int, []),
+    "hp_tx_status": (C.c_int, [_CtxP]),
     "hp_host_alloc": (C.c_void_p, [C.c_size_t]),
     "hp_host_free": (None, [C.c_void_p]),
 }
@@ -176,6 +178,11 @@ def smem_optin(kernel_id: int, device: int) -> int:
     out = C.c_int()
     check(load().hp_smem_optin(kernel_id, device, C.byref(out)), "hp_smem_optin")
     return out.value
+
+
+def last_two_step_kernel() -> str:
+    """Which kernel the most recent two-step pass launched (process-wide)."""
+    return {0: "none", 1: "k_stencil_tb2", 2: "k_stencil_tx"}[int(load().hp_last_two_step_kernel())]
 
 
 def last_error() -> str:
@@ -284,6 +291,10 @@ class Context:
         out = C.c_double()
         check(self.lib.hp_read_gosa(self.ptr, side, C.byref(out)), "hp_read_gosa")
         return out.value
+
+    def tx_status(self) -> int:
+        """1 if an exchange-kernel launch of this context timed out (never expected)."""
+        return check(self.lib.hp_tx_status(self.ptr), "hp_tx_status")
 
     def init_device(self) -> None:
         check(self.lib.hp_init_device(self.ptr), "hp_init_device")

@@ -527,3 +527,60 @@ def test_l_grid_slabs_bit_exact(gpu, l_oracle_n4, ranks, tb):
             assert abs(gosa - want_g) <= 1e-11 * want_g, (ranks, tb, nn)
     finally:
         lib.hp_set_temporal_blocking(old)
+
+
+# --- the tile-exchange two-step kernel (k_stencil_tx) ----------------------------------
+
+@pytest.mark.parametrize("dims,nn,minchunk", [
+    ((75, 45, 141), 4, 0),     # 2 x 6 tiles, ragged j and k
+    ((75, 45, 141), 5, 8),     # several plane chunks, odd nn (one single-step pass)
+    ((37, 21, 70), 4, 4),      # one k-tile, 3 j-tiles, 4-plane chunks
+    ((20, 17, 300), 3, 4),     # 3 k-tiles, j extent a multiple of the tile rows
+    ((6, 6, 6), 2, 0),         # 3 interior planes, one tile
+    ((129, 129, 257), 4, 0),   # M: 2 x 18 tiles x 4 chunks
+])
+def test_exchange_kernel_bit_exact(gpu, monkeypatch, dims, nn, minchunk):
+    """k_stencil_tx (tiles exchange their p1 boundary through L2 instead of recomputing
+    a halo) forced on small and ragged grids, several plane chunks: p bit-exact with the
+    oracle, gosa within 1e-12, and the launch really was the exchange kernel."""
+    sz = himeno.custom_size(*dims)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    monkeypatch.setenv("HIMENO_TX", "2")
+    if minchunk:
+        monkeypatch.setenv("HIMENO_TX_MINCHUNK", str(minchunk))
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(1)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+            assert N.last_two_step_kernel() == "k_stencil_tx"
+            assert ctx.tx_status() == 0
+            kt = ctx.time_jacobi(nn, 1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    assert kt.stencil_iters == nn / ((nn + 1) // 2)    # two-step passes + odd remainder
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * max(ref["gosa64"], 1e-300)
+
+
+def test_exchange_kernel_matches_tb2_on_L(gpu, monkeypatch):
+    """On the headline grid the exchange kernel's policy (HIMENO_TX=1) selects it -- 148
+    tiles of 128 x 7 points, one per SM -- and it matches k_stencil_tb2 (the default,
+    HIMENO_TX unset) bit for bit, with no neighbour-wait timeout."""
+    sz = himeno.size("L")
+    with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+        monkeypatch.setenv("HIMENO_TX", "1")
+        ctx.init_device()
+        ctx.jacobi_device(4, 1)
+        assert N.last_two_step_kernel() == "k_stencil_tx"
+        assert ctx.tx_status() == 0
+        p_tx, g_tx = ctx.read_field("p", 1), ctx.read_gosa(1)
+        monkeypatch.delenv("HIMENO_TX")
+        ctx.init_device()
+        ctx.jacobi_device(4, 1)
+        assert N.last_two_step_kernel() == "k_stencil_tb2"
+        p_tb, g_tb = ctx.read_field("p", 1), ctx.read_gosa(1)
+    assert np.array_equal(p_tx, p_tb)
+    assert abs(g_tx - g_tb) <= 1e-12 * g_tb

@@ -221,7 +221,8 @@ typedef struct hp_kernel_times {
   double total_ms;        /* first to last event of the call                 */
   double stencil_ms;      /* mean duration of one stencil launch (pass)       */
   double other_ms;        /* mean duration of the other launches (copies)     */
-  double stencil_iters;   /* mean Jacobi iterations per stencil pass (1 or 2) */
+  double stencil_iters;   /* mean Jacobi iterations per stencil launch: 1, 2 (two-step
+                             pass) or all pairs of a flow launch (stencil_flow_ok) */
   int32_t n_stencil, n_other;
 } hp_kernel_times;
 int hp_time_steps(hp_ctx* ctx, int steps, int nn, int variant, double* ms_out);
@@ -259,9 +260,10 @@ int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
  * two-step tile-exchange kernel).  The library raises it per device before the
  * first launch there. */
 int hp_smem_optin(int id, int device, int* bytes);
-/* Diagnostics: the kernel the most recent two-step pass (any context) launched:
- * 0 none yet, 1 k_stencil_tb2 (halo-recomputing tiles), 2 k_stencil_tx (tiles
- * exchanging their p1 boundary through L2). */
+/* Diagnostics: the kernel the most recent two-step launch (any context) used:
+ * 0 none yet, 1 k_stencil_tb2 (halo-recomputing tiles, one pass), 2 k_stencil_tx
+ * (tiles exchanging their p1 boundary through L2), 3 k_stencil_tb2 running several
+ * passes in one flow launch (the device time loop's default for nn >= 4). */
 int hp_last_two_step_kernel(void);
 /* Diagnostics: 1 if an exchange-kernel launch of this context ever timed out
  * waiting for a neighbour tile (its results are invalid and gosa was set to NaN),

@@ -1302,9 +1302,12 @@ extern "C" int hp_time_jacobi(hp_ctx* c, int nn, int variant, hp_kernel_times* o
       // one pass at a time (same choice as stencil_iterations), an event after each
       float* last = nullptr;
       int passes = 0;
-      // one pass as stencil_iterations would launch it: two iterations only when
-      // temporal blocking is on (otherwise each single-step launch is timed alone)
-      const int step = (nn - it >= 2 && set_temporal_blocking(-1)) ? 2 : 1;
+      // one launch as stencil_iterations would make it: every remaining pair of
+      // iterations in one flow launch where that applies, else two iterations per
+      // pass when temporal blocking is on (otherwise each single step alone)
+      const bool tb = set_temporal_blocking(-1) != 0;
+      int step = (nn - it >= 2 && tb) ? 2 : 1;
+      if (tb && nn - it >= 4 && stencil_flow_ok(c->dev, a, device_sm_count())) step = (nn - it) / 2 * 2;
       ok = stencil_iterations(c->dev, cur, oth, step, a, c->sink(), c->stream, &last, &passes) >= 0;
       ok = ok && mark();   // (a 2-step request may have run as two single passes)
       is_stencil.push_back(1);

@@ -111,6 +111,16 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
 // two Jacobi iterations per pass (temporal blocking); 0 = not applicable
 int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
                        const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms);
+// `passes` >= 2 two-step passes in ONE launch (units of pass t+1 start as soon as
+// their neighbourhood in pass t is done); result in p_out if passes is odd, else
+// p_in; 0 = not applicable (caller launches pass by pass)
+int launch_stencil_flow(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                        int passes, const LaunchArgs& a, const GosaSink& g, cudaStream_t s,
+                        int sms);
+// 1 if the device time loop of this geometry runs its two-step passes as one flow
+// launch (policy of launch_stencil_flow), else 0
+int stencil_flow_ok(const DevFields& F, const LaunchArgs& a, int sms);
+int device_sm_count();   // kernels.cu
 // run iterations [0, nn) p_in -> ... choosing one- or two-step passes; sets
 // *last to the buffer holding p_nn; returns kernels launched or -1
 int stencil_iterations(const DevFields& F, float* buf0, float* buf1, int nn, const LaunchArgs& a,

@@ -493,6 +493,8 @@ int launch_nest(Nest nest, Mapping map, const DevFields& F, const Box& box,
   }
 }
 
+int device_sm_count() { return sm_count(); }
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -550,6 +552,22 @@ int stencil_iterations(const DevFields& F, float* buf0, float* buf1, int nn, con
   float* cur = buf0;
   float* oth = buf1;
   int n = 0, it = 0;
+  if (g_temporal_blocking && nn - it >= 4) {
+    // every two-step pass in one flow launch (stencil_tma.cu)
+    const int passes = (nn - it) / 2;
+    const int r = launch_stencil_flow(F, F.tma, cur, oth, passes, a, g, s, sm_count());
+    if (r < 0) return -1;
+    if (r > 0) {
+      n += r;
+      it += 2 * passes;
+      if (stencil_launches) ++*stencil_launches;
+      if (passes & 1) {   // the last pass wrote oth
+        float* t = cur;
+        cur = oth;
+        oth = t;
+      }
+    }
+  }
   while (it < nn) {
     int r = 0;
     if (g_temporal_blocking && nn - it >= 2) {

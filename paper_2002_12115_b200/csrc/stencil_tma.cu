@@ -198,7 +198,9 @@ k_stencil_tma(const __grid_constant__ StencilMaps maps, DevFields F, float* __re
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
       if (u == kNoUnit) break;
-      units.decode(u, s);
+      units.decode(u % units.count, s);
+      const int pass = (int)(u / units.count);
+      (void)pass;
       const int j = j_lo + s.jt * TJ + warp;
       const bool row_ok = j < j_hi;
       const int kb = s.kt * TK + lane * 4;
@@ -338,7 +340,22 @@ constexpr int kTb2Shapes = 4;
 
 struct __align__(64) Tb2Maps {
   CUtensorMap coef[NCOEF];   // box QK x R1, origin (k0-4, j0-1)
-  CUtensorMap pin;           // box QK+8 x (R1+2), origin (k0-8, j0-2)
+  CUtensorMap pin;           // box QK+8 x (R1+2), origin (k0-8, j0-2): input of even passes
+  CUtensorMap pin2;          // the same over the other buffer: input of odd passes (flow)
+};
+
+// Several two-step passes in one launch ("flow"): the unit queue is pass-major and
+// a unit of pass t (t >= 1) starts once the pass t-1 units of its 3 x 3 tile
+// neighbourhood that cover its planes +-2 have completed (per-unit completion tags):
+// pass t+1 overlaps the tail of pass t instead of waiting for the whole grid.  The
+// dependencies of a unit are claimed before it (pass-major order) by running CTAs,
+// so every wait ends.  passes == 1: one classic pass (no tags).
+struct Flow {
+  int passes;          // two-step passes in this launch
+  int upp;             // units per pass
+  float* out[2];       // pass t writes out[t & 1] (and reads the other buffer)
+  unsigned* done;      // [upp]: unit v of pass t complete <=> done[v] >= tag0 + t + 1
+  unsigned tag0;       // launch epoch * 4096
 };
 
 // p0 tile row (PW0 floats): sub-lane quad at column 4 + 4*hl (k0-4+4*hl), edges at
@@ -614,11 +631,31 @@ __device__ __forceinline__ void tmem_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// End of a unit for the step-2 warps of a two-step kernel: the gosa partial of the
+// last pass's units (only the last iteration's gosa is observable), and in a flow
+// launch the unit's completion tag, published after every step-2 thread's stores
+// (named barrier, then a gpu-scope fence by the publishing thread).
+__device__ void unit_finish(const GosaSink& g, uint32_t u, uint32_t upp, const Flow& fl, double v,
+                            double* part, int wrel, int nw, int bar) {
+  const uint32_t pass = u / upp, local = u % upp;
+  if ((int)pass == fl.passes - 1) {
+    unit_partial(g, local, v, part, wrel, nw, bar);
+  } else {
+    named_bar_sync(bar, nw * 32);
+  }
+  if (fl.passes > 1 && wrel == 0 && (threadIdx.x & 31) == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fl.done + local),
+                 "r"(fl.tag0 + pass + 1u)
+                 : "memory");
+  }
+}
+
 template <int LW, int NW1_, int SC_, bool ST_ = false>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
-k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restrict__ out,
-              int i_lo, int i_hi, int j_lo, int j_hi, int k_lo, int k_hi, int k_org, int ktiles,
-              int chunk, int full, int g_lo, int g_hi, float omega, GosaSink g, int reset) {
+k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i_hi, int j_lo,
+              int j_hi, int k_lo, int k_hi, int k_org, int ktiles, int chunk, int full, int g_lo,
+              int g_hi, float omega, GosaSink g, int reset, Flow fl) {
   using T = Tb2<LW, NW1_, SC_>;
   constexpr int RPW = T::RPW, NW1 = T::NW1, NW2 = T::NW2, R1 = T::R1, TJ2 = T::TJ2,
                 QK = T::QK, TK2 = T::TK2, SC = T::SC;
@@ -644,6 +681,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
   const Units units(ni, ktiles, ktiles * jtiles, chunk, full);
+  const uint32_t nunits = units.count * (uint32_t)fl.passes;   // queue: pass-major
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
     for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], NW1 + NW2); }
@@ -667,20 +705,60 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
   double acc = 0.0;
   if (warp == NW1 + NW2) {
     // ------------------------------------------------------------- producer
-    if (lane == 0) {
-      uint32_t sp = 0, sc = 0;
-      Unit s{0, 0, 0, 0};
-      for (uint32_t n = 0;; ++n) {
-        const uint32_t u = unit_publish(ring, n, g.work, units.count);
-        if (u == kNoUnit) break;
-        units.decode(u, s);
+    // lane 0 claims units and issues the TMA loads; in a flow launch the whole warp
+    // first waits for the unit's dependencies (one completion tag per lane)
+    uint32_t sp = 0, sc = 0;
+    Unit s{0, 0, 0, 0};
+    for (uint32_t n = 0;; ++n) {
+      uint32_t u = 0;
+      if (lane == 0) u = unit_publish(ring, n, g.work, nunits);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u == kNoUnit) break;
+      const int pass = (int)(u / units.count);
+      units.decode(u % units.count, s);
+      if (pass > 0) {
+        // lane l: neighbour tile l / 3 of the 3 x 3 block, l % 3-th plane chunk
+        // overlapping [ia-2, ib+2) (planes the step-1 box reads, and the planes this
+        // unit overwrites in the buffer the previous pass read)
+        bool ok = true;
+        const int d = lane / 3, co = lane % 3;
+        if (d < 9) {
+          const int jn = s.jt + d / 3 - 1, kn = s.kt + d % 3 - 1;
+          if (jn >= 0 && jn < jtiles && kn >= 0 && kn < ktiles) {
+            const int tn = jn * ktiles + kn;
+            int v = -1;
+            if (tn < units.full) {
+              if (co == 0) v = tn;
+            } else {
+              const int c_lo = max(0, s.ia - 2) / units.len;
+              const int c_hi = min(ni - 1, s.ib + 1) / units.len;
+              if (c_lo + co <= c_hi)
+                v = units.full + (c_lo + co) * (units.tiles - units.full) + (tn - units.full);
+            }
+            if (v >= 0) {
+              const unsigned want = fl.tag0 + (unsigned)pass;   // pass - 1 complete
+              uint32_t polls = 0;
+              while (ld_acquire_u32(fl.done + v) < want) {
+                if (++polls > (1u << 26)) asm volatile("trap;");
+              }
+            }
+          }
+        }
+        (void)ok;
+        __syncwarp();
+        // the previous pass's generic-proxy stores before this CTA's TMA (async
+        // proxy) reads of them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (lane == 0) {
         const int ia = i_lo + s.ia, ib = i_lo + s.ib;
         const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
+        const CUtensorMap* pin = (pass & 1) ? &maps.pin2 : &maps.pin;
         auto load_p0 = [&](int plane) {
           const int slot = sp % SP;
           if (sp >= (uint32_t)SP) mbar_wait(&pempty[slot], ((sp / SP) - 1) & 1);
           mbar_expect_tx(&pfull[slot], T::kP0Bytes);
-          tma_load_3d(p0ring + slot * T::kP0Slot, &maps.pin, &pfull[slot], k0 - 8, j0 - 2, plane);
+          tma_load_3d(p0ring + slot * T::kP0Slot, pin, &pfull[slot], k0 - 8, j0 - 2, plane);
           ++sp;
         };
         load_p0(ia - 2);
@@ -696,6 +774,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
           ++sc;
         }
       }
+      __syncwarp();
     }
   } else if (warp < NW1) {
     // ------------------------------------- step-1 warps (tile row r = j0-1+r)
@@ -707,7 +786,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
       if (u == kNoUnit) break;
-      units.decode(u, s);
+      units.decode(u % units.count, s);
+      const int pass = (int)(u / units.count);
+      (void)pass;
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
       const int j1 = j0 - 1 + r;
@@ -788,7 +869,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
       if (u == kNoUnit) break;
-      units.decode(u, s);
+      units.decode(u % units.count, s);
+      const int pass = (int)(u / units.count);
+      (void)pass;
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
       const int j = j0 + r2;
@@ -852,7 +935,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
             if (writer && in2[x]) acc += (double)fmul(ss[x], ss[x]);
           }
           if (writer) {
-            float* o = out + F.at(m - 1, j, kq);
+            float* o = ((pass & 1) ? fl.out[1] : fl.out[0]) + F.at(m - 1, j, kq);
             if (in2[0] && in2[1] && in2[2] && in2[3]) {
               *reinterpret_cast<float4*>(o) = make_float4(w[0], w[1], w[2], w[3]);
             } else {
@@ -864,7 +947,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
         ym = zm; y0 = z0; yp = zp;
         zm = nm; z0 = n0; zp = np;
       }
-      unit_partial(g, u, acc, unit_part, warp - NW1, NW2, 1);
+      unit_finish(g, u, units.count, fl, acc, unit_part, warp - NW1, NW2, 1);
       acc = 0.0;
     }
   } else {
@@ -875,7 +958,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
     for (uint32_t n = 0;; ++n) {
       const uint32_t u = unit_take(ring, n, lane);
       if (u == kNoUnit) break;
-      units.decode(u, s);
+      units.decode(u % units.count, s);
+      const int pass = (int)(u / units.count);
+      (void)pass;
       const int ia = i_lo + s.ia, ib = i_lo + s.ib;
       const int k0 = k_org + s.kt * TK2, j0 = j_lo + s.jt * TJ2;
       const int j = j0 + r2;
@@ -912,7 +997,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
           __syncwarp();
           if (lane == 0) mbar_arrive(&cempty[cslot]);
           if (writer) {
-            float* o = out + F.at(m - 1, j, kq);
+            float* o = ((pass & 1) ? fl.out[1] : fl.out[0]) + F.at(m - 1, j, kq);
             if (in2[0] && in2[1] && in2[2] && in2[3]) {
               *reinterpret_cast<float4*>(o) = make_float4(w[0], w[1], w[2], w[3]);
             } else {
@@ -930,7 +1015,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, float* __restri
       }
       // stage of plane ib carries no output plane either
       if (lane == 0) mbar_arrive(&cempty[(sc - 1) % SC]);
-      unit_partial(g, u, acc, unit_part, warp - NW1, NW2, 1);
+      unit_finish(g, u, units.count, fl, acc, unit_part, warp - NW1, NW2, 1);
       acc = 0.0;
     }
   }
@@ -967,6 +1052,10 @@ struct TmaState {
   unsigned* err = nullptr;
   int tx_ktiles = 0, tx_jtiles = 0, tx_chunks = 0;   // capacity (0: exchange kernel off)
   unsigned epoch = 0;
+  // multi-pass flow launches of k_stencil_tb2: per-unit completion tags
+  unsigned* done = nullptr;
+  int done_cap = 0;
+  unsigned flow_epoch = 0;
 };
 
 }  // namespace
@@ -1023,6 +1112,19 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
     delete t;
     return nullptr;
   }
+  // completion tags of the flow launches: one per unit of a pass (at most the gosa
+  // partial capacity, which launch_tb2 enforces)
+  {
+    const int cap = gosa_capacity_needed(F);
+    if (cudaMalloc(&t->done, (size_t)cap * 4) == cudaSuccess &&
+        cudaMemset(t->done, 0, (size_t)cap * 4) == cudaSuccess) {
+      t->done_cap = cap;
+    } else {
+      if (t->done) cudaFree(t->done);
+      t->done = nullptr;
+      cudaGetLastError();   // no flow launches for this context
+    }
+  }
   // exchange buffers for the j/k extents of this context (slab contexts share the
   // global j/k extents): tiles of 128 k x TJ j over [0, K-2) x [1, J-2), only when
   // every tile can be resident at once
@@ -1058,6 +1160,7 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
 void destroy_stencil_tma(void* h) {
   TmaState* t = static_cast<TmaState*>(h);
   if (!t) return;
+  if (t->done) cudaFree(t->done);
   if (t->xr) cudaFree(t->xr);
   if (t->xc) cudaFree(t->xc);
   if (t->err) cudaFree(t->err);
@@ -1247,7 +1350,7 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
 }
 
 template <int LW, int NW1, int SC, bool ST = false>
-static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int i_lo, int i_hi,
+static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo, int i_hi,
                       int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
                       int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
   using T = Tb2<LW, NW1, SC>;
@@ -1258,8 +1361,9 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   if (full < 0 || full > tiles) full = 0;
   const long long units = full + (tiles - full) * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
-  if (grid > units) grid = units;
-  if (units > g.capacity) return -1;   // one gosa partial per unit
+  if (grid > units * fl.passes) grid = units * fl.passes;
+  if (units > g.capacity) return -1;   // one gosa partial per unit (of the last pass)
+  fl.upp = (int)units;
   const size_t smem = T::smem_bytes();
   // the work-queue counter is zero: set at context creation, reset by the last CTA
   if (!ensure_smem_optin((const void*)k_stencil_tb2<LW, NW1, SC, ST>, (int)smem)) return -1;
@@ -1274,9 +1378,9 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, float* p_out, int
   cfg.stream = s;
   cfg.attrs = la;
   cfg.numAttrs = pdl ? 1 : 0;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC, ST>, maps, F, p_out, i_lo,
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC, ST>, maps, F, i_lo,
                                            i_hi, j_lo, j_hi, k_lo, k_hi, k_org, ktiles, chunk, full,
-                                           g_lo, g_hi, a.omega, g, a.gosa_reset);
+                                           g_lo, g_hi, a.omega, g, a.gosa_reset, fl);
   return e == cudaSuccess ? 1 : -1;
 }
 
@@ -1390,8 +1494,9 @@ static int launch_tx(TmaState* t, const DevFields& F, const float* p_in, float* 
   return e == cudaSuccess ? 1 : -1;
 }
 
-// which two-step kernel the last two-step pass launched: 1 = k_stencil_tb2,
-// 2 = k_stencil_tx (hp_last_two_step_kernel; tests and bench.py name it)
+// which two-step kernel the last two-step launch used: 1 = k_stencil_tb2 (one
+// pass), 2 = k_stencil_tx, 3 = k_stencil_tb2 in a multi-pass flow launch
+// (hp_last_two_step_kernel; tests and bench.py name it)
 static std::atomic<int> g_last_two_step{0};
 
 int tx_error(const void* h) {
@@ -1402,12 +1507,14 @@ int tx_error(const void* h) {
   return v ? 1 : 0;
 }
 
-// Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not
-// applicable: caller runs two single steps), or -1 on launch error.
-int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
-                       const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
-  const TmaState* t = static_cast<const TmaState*>(h);
-  if (!t || (p_in != t->p && p_in != t->scratch)) return 0;
+// `passes` two-step passes p_in -> p_out -> p_in ... (2 * passes Jacobi iterations)
+// in one launch; the result is in p_out for an odd number of passes, p_in for an
+// even one.  Returns 1, 0 (not applicable: the caller runs single steps), or -1.
+static int launch_two_step(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                           int passes, const LaunchArgs& a, const GosaSink& g, cudaStream_t s,
+                           int sms) {
+  TmaState* t = const_cast<TmaState*>(static_cast<const TmaState*>(h));
+  if (!t || (p_in != t->p && p_in != t->scratch) || passes < 1) return 0;
   const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
             k_hi = a.kmax - 1;
   // step 1 reads p0 two planes beyond the planes it updates: the full grid (plane
@@ -1416,27 +1523,54 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
   if (!full && (i_lo < 2 || i_hi > F.I - 2)) return 0;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
   const int g_lo = 1 - a.i_off, g_hi = a.imax - 1 - a.i_off;
-  // the exchange kernel when this geometry's tiles can all be resident
-  {
-    const int r = launch_tx(const_cast<TmaState*>(t), F, p_in, p_out, i_lo, i_hi, j_lo, j_hi,
-                            k_lo, k_hi, g_lo, g_hi, a, g, s, sms);
+  if (passes > 1 && !t->done) return 0;
+  // the exchange kernel (one pass per launch) when enabled and its tiles can all
+  // be resident
+  if (passes == 1) {
+    const int r = launch_tx(t, F, p_in, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, a, g,
+                            s, sms);
     if (r != 0) {
       g_last_two_step = 2;
       return r;
     }
   }
-  g_last_two_step = 1;
-  const Tb2Choice c = tb2_choose(i_hi - i_lo, j_hi - j_lo, k_hi, sms);
+  g_last_two_step = passes > 1 ? 3 : 1;
+  Tb2Choice c = tb2_choose(i_hi - i_lo, j_hi - j_lo, k_hi, sms);
   const int v = c.shape;
   Tb2Maps maps = t->tb2[v];
-  if (p_in == t->scratch) maps.pin = t->tb2_scratch[v];
+  const bool from_scratch = p_in == t->scratch;
+  maps.pin = from_scratch ? t->tb2_scratch[v] : t->tb2[v].pin;
+  maps.pin2 = from_scratch ? t->tb2[v].pin : t->tb2_scratch[v];
+  Flow fl{};
+  fl.passes = passes;
+  fl.out[0] = p_out;
+  fl.out[1] = const_cast<float*>(p_in);
+  if (passes > 1) {
+    // a unit of pass t+1 waits for whole neighbouring units of pass t: chunked units
+    // only (whole columns would make every wait a wait for the entire pass)
+    c.full = 0;
+    // balanced chunks of about 22 planes (M, 126 planes: 6 x 21 -> 43.8 us per pass;
+    // 16 -> 45.6, 22 -> 44.1, 24 -> 44.6, 32 -> 48.7; profiles/r02_flow.md)
+    const int fc = env_int("HIMENO_FLOW_CHUNK");
+    const int ni = i_hi - i_lo;
+    const int nch = std::max(1, (ni + 11) / 22);
+    c.chunk = fc > 0 ? fc : (ni + nch - 1) / nch;
+    fl.done = t->done;
+    std::lock_guard<std::mutex> lock(g_tx_mu);
+    if (++t->flow_epoch >= (1u << 20) - 1u) {   // tags epoch * 4096 + pass + 1 in 32 bits
+      if (cudaMemsetAsync(t->done, 0, (size_t)t->done_cap * 4, s) != cudaSuccess) return -1;
+      t->flow_epoch = 1;
+    }
+    if (passes >= 4095) return 0;
+    fl.tag0 = t->flow_epoch * 4096u;
+  }
 #define HP_TB2(LW, NW1, SC) \
-  launch_tb2<LW, NW1, SC>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, c.chunk, \
+  launch_tb2<LW, NW1, SC>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, c.chunk, \
                           c.full, a, g, s, sms)
   switch (v) {
     case 1:
       if (env_int("HIMENO_TB2_STASH") != 0)
-        return launch_tb2<16, 8, 4, true>(maps, F, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo,
+        return launch_tb2<16, 8, 4, true>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo,
                                           g_hi, c.chunk, c.full, a, g, s, sms);
       return HP_TB2(16, 8, 4);
     case 2: return HP_TB2(16, 6, 5);
@@ -1444,6 +1578,44 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
     default: return HP_TB2(32, 8, 4);
   }
 #undef HP_TB2
+}
+
+// Two-step pass p_in -> p_out (2 Jacobi iterations); returns 1, 0 (not
+// applicable: caller runs two single steps), or -1 on launch error.
+int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                       const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+  return launch_two_step(F, h, p_in, p_out, 1, a, g, s, sms);
+}
+
+// Flow launches pay where the per-pass drain matters: when one pass's tiles fit in
+// one wave of the SMs (M: 45 tiles, 50.1 -> 44.6 us per pass); with more tiles (L:
+// 190, whole tile columns) the pass-by-pass launches are as fast or faster
+// (profiles/r02_flow.md).  HIMENO_TB2_FLOW: 0 = never, 1 = always, unset = that rule.
+int stencil_flow_ok(const DevFields& F, const LaunchArgs& a, int sms) {
+  const TmaState* t = static_cast<const TmaState*>(F.tma);
+  if (!t || !t->done) return 0;
+  const int mode = env_int("HIMENO_TB2_FLOW");
+  if (mode == 0 || env_int("HIMENO_TX") > 0) return 0;
+  if (mode < 0) {
+    const int j_hi = a.jmax - 1, k_hi = a.kmax - 1;
+    const Tb2Choice c = tb2_choose(a.li_hi - a.li_lo, j_hi - 1, k_hi, sms);
+    long long tiles = 0;
+    switch (c.shape) {
+      case 0: tiles = tb2_tiles<32, 8, 4>(j_hi - 1, k_hi); break;
+      case 1: tiles = tb2_tiles<16, 8, 4>(j_hi - 1, k_hi); break;
+      case 2: tiles = tb2_tiles<16, 6, 5>(j_hi - 1, k_hi); break;
+      default: tiles = tb2_tiles<16, 5, 6>(j_hi - 1, k_hi); break;
+    }
+    if (tiles > sms) return 0;
+  }
+  return 1;
+}
+
+int launch_stencil_flow(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                        int passes, const LaunchArgs& a, const GosaSink& g, cudaStream_t s,
+                        int sms) {
+  if (h != F.tma || !stencil_flow_ok(F, a, sms)) return 0;
+  return launch_two_step(F, h, p_in, p_out, passes, a, g, s, sms);
 }
 
 }  // namespace hp

@@ -182,7 +182,8 @@ def smem_optin(kernel_id: int, device: int) -> int:
 
 def last_two_step_kernel() -> str:
     """Which kernel the most recent two-step pass launched (process-wide)."""
-    return {0: "none", 1: "k_stencil_tb2", 2: "k_stencil_tx"}[int(load().hp_last_two_step_kernel())]
+    return {0: "none", 1: "k_stencil_tb2", 2: "k_stencil_tx",
+            3: "k_stencil_tb2 (flow)"}[int(load().hp_last_two_step_kernel())]
 
 
 def last_error() -> str:

@@ -106,6 +106,41 @@ static int pass_step(int done, int nn) {
   return (set_temporal_blocking(-1) && nn - done >= 2) ? 2 : 1;
 }
 
+// Halo exchange overlapped with the interior (HIMENO_DD_OVERLAP=0 turns it off):
+// a two-step pass runs as (1) the slab's two boundary plane pairs, then an event,
+// then (2) the interior; the exchange of pass t waits only for (1) and runs on a
+// comm stream while (2) computes; pass t+1 waits for it before its own (1) -- its
+// interior needs only the slab's own planes.  SMs left free for NCCL's kernels
+// during (2): HIMENO_DD_RESERVE (default 8; copy-engine peer copies need none).
+static int dd_overlap() {
+  const char* e = getenv("HIMENO_DD_OVERLAP");   // read per call (tests switch it)
+  return e ? atoi(e) : 1;
+}
+static int dd_reserve() {
+  const char* e = getenv("HIMENO_DD_RESERVE");
+  return e ? atoi(e) : 8;
+}
+
+// One pass on a slab, split into boundary + interior when overlapping; `bdone` is
+// recorded on the compute stream after the planes the neighbours need are written.
+static int slab_pass_overlapped(hp_ctx* c, const float* in, float* out, int step,
+                                const LaunchArgs& a, bool overlap, int reserve, cudaEvent_t bdone) {
+  if (overlap && step == 2) {
+    const int r1 = launch_stencil_tb2_part(c->dev, c->dev.tma, in, out, a, c->sink(), c->stream,
+                                           sm_count_of(c), 1, 0);
+    if (r1 < 0) return -1;
+    if (r1 > 0) {
+      if (cudaEventRecord(bdone, c->stream) != cudaSuccess) return -1;
+      const int r2 = launch_stencil_tb2_part(c->dev, c->dev.tma, in, out, a, c->sink(), c->stream,
+                                             sm_count_of(c), 2, reserve);
+      return r2 > 0 ? 2 : -1;
+    }
+  }
+  const int r = slab_pass(c, in, out, step, a);
+  if (r < 0) return -1;
+  return cudaEventRecord(bdone, c->stream) == cudaSuccess ? r : -1;
+}
+
 extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
   if (!ctxs || n < 1 || nn < 0) {
     set_error("hp_group_jacobi: bad arguments");
@@ -121,15 +156,19 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
       return HP_ERR_ARG;
     }
   }
-  std::vector<cudaEvent_t> done(n, nullptr);
+  std::vector<cudaEvent_t> done(n, nullptr), hin(n, nullptr);
+  std::vector<cudaStream_t> comm(n, nullptr);
   int rc = HP_OK;
   auto fail = [&](cudaError_t e, const char* what) {
     if (rc == HP_OK) rc = cuda_fail(e, what);
   };
+  const bool overlap = dd_overlap() != 0 && n > 1;
   for (int r = 0; r < n && rc == HP_OK; ++r) {
     cudaSetDevice(ctxs[r]->device);
     cudaError_t e = cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming);
-    if (e != cudaSuccess) fail(e, "event create");
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hin[r], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&comm[r], cudaStreamNonBlocking);
+    if (e != cudaSuccess) fail(e, "event / stream create");
     else if (time_loop_begin(ctxs[r], ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "begin");
   }
   int pass = 0;
@@ -138,16 +177,23 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     for (int r = 0; r < n && rc == HP_OK; ++r) {
       hp_ctx* c = ctxs[r];
       cudaSetDevice(c->device);
-      if (slab_pass(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, ctx_args(c, 1)) < 0)
-        fail(cudaGetLastError(), "stencil pass");
-      c->launches++;
-      cudaError_t e = cudaEventRecord(done[r], c->stream);
-      if (e != cudaSuccess) fail(e, "event record");
+      // the halos of the previous pass, before this pass's boundary planes
+      if (pass > 0 && n > 1) {
+        cudaError_t e = cudaStreamWaitEvent(c->stream, hin[r], 0);
+        if (e != cudaSuccess) fail(e, "wait halo");
+      }
+      const int k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step,
+                                         ctx_args(c, 1), overlap, 0, done[r]);
+      if (k < 0) fail(cudaGetLastError(), "stencil pass");
+      c->launches += k > 0 ? k : 0;
     }
-    for (int r = 0; r < n && rc == HP_OK; ++r) {
+    // halo planes on each receiver's comm stream (copy engines), after the
+    // receiver's and the sender's boundary planes of this pass
+    for (int r = 0; r < n && rc == HP_OK && n > 1; ++r) {
       hp_ctx* c = ctxs[r];
       cudaSetDevice(c->device);
       float* out = pass_buffer(c, pass + 1);
+      cudaError_t e = cudaStreamWaitEvent(comm[r], done[r], 0);   // WAR: this pass's reads
       for (int side = -1; side <= 1 && rc == HP_OK; side += 2) {
         const int q = r + side;
         if (q < 0 || q >= n) continue;
@@ -156,15 +202,22 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
         // lower halo <- neighbour's last two interior planes; upper <- its first two
         const int dst_plane = side < 0 ? c->li_lo - kHalo : c->li_hi;
         const int src_plane = side < 0 ? nb->li_hi - kHalo : nb->li_lo;
-        cudaError_t e = cudaStreamWaitEvent(c->stream, done[q], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(comm[r], done[q], 0);
         if (e == cudaSuccess)
           e = cudaMemcpyPeerAsync(plane_ptr(c, out, dst_plane), c->device,
                                   plane_ptr(nb, nb_out, src_plane), nb->device,
-                                  kHalo * plane_bytes(c), c->stream);
+                                  kHalo * plane_bytes(c), comm[r]);
         if (e != cudaSuccess) fail(e, "halo copy");
       }
+      if (e == cudaSuccess) e = cudaEventRecord(hin[r], comm[r]);
+      if (e != cudaSuccess) fail(e, "halo event");
     }
     it += step;
+  }
+  for (int r = 0; r < n && rc == HP_OK && n > 1 && pass > 0; ++r) {
+    cudaSetDevice(ctxs[r]->device);
+    cudaError_t e = cudaStreamWaitEvent(ctxs[r]->stream, hin[r], 0);
+    if (e != cudaSuccess) fail(e, "wait halo");
   }
   for (int r = 0; r < n && rc == HP_OK; ++r) {
     cudaSetDevice(ctxs[r]->device);
@@ -183,8 +236,15 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     if (e != cudaSuccess) fail(e, "gosa partial");
     total += nn > 0 ? part : 0.0;
   }
-  for (int r = 0; r < n; ++r)
+  for (int r = 0; r < n; ++r) {
+    cudaSetDevice(ctxs[r]->device);
+    if (comm[r]) {
+      cudaStreamSynchronize(comm[r]);
+      cudaStreamDestroy(comm[r]);
+    }
     if (done[r]) cudaEventDestroy(done[r]);
+    if (hin[r]) cudaEventDestroy(hin[r]);
+  }
   if (rc == HP_OK && gosa_out) *gosa_out = total;
   return rc;
 }
@@ -237,6 +297,9 @@ Nccl* nccl() {
 struct DD {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  cudaStream_t xs = nullptr;      // halo exchange stream (overlapped with the interior)
+  cudaEvent_t bdone = nullptr;    // boundary planes of the current pass written
+  cudaEvent_t hin = nullptr;      // halos of the current pass received
 };
 
 int nccl_fail(ncclResult_t r, const char* what) {
@@ -249,6 +312,12 @@ int nccl_fail(ncclResult_t r, const char* what) {
 void hp::dd_destroy(hp_ctx* c) {
   DD* d = static_cast<DD*>(c->dd);
   if (d && d->comm && nccl()) nccl()->CommDestroy(d->comm);
+  if (d && d->xs) {
+    cudaStreamSynchronize(d->xs);
+    cudaStreamDestroy(d->xs);
+  }
+  if (d && d->bdone) cudaEventDestroy(d->bdone);
+  if (d && d->hin) cudaEventDestroy(d->hin);
   delete d;
   c->dd = nullptr;
 }
@@ -297,6 +366,14 @@ extern "C" int hp_dd_init(hp_ctx* c, int nranks, int rank, const unsigned char* 
       return nccl_fail(r, "ncclCommInitRank");
     }
   }
+  cudaSetDevice(c->device);
+  if (cudaStreamCreateWithFlags(&d->xs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&d->bdone, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&d->hin, cudaEventDisableTiming) != cudaSuccess) {
+    c->dd = d;
+    dd_destroy(c);
+    return cuda_fail(cudaGetLastError(), "hp_dd_init streams");
+  }
   c->dd = d;
   return HP_OK;
 }
@@ -314,35 +391,48 @@ extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
   const LaunchArgs a = ctx_args(c, 1);
   if (time_loop_begin(c, a) < 0) return cuda_fail(cudaGetLastError(), "begin");
   const size_t count = kHalo * c->dev.plane();
+  const bool overlap = dd_overlap() != 0 && l && d->nranks > 1;
+  const int reserve = overlap ? dd_reserve() : 0;
   int pass = 0;
   for (int it = 0; it < nn; ++pass) {
     const int step = pass_step(it, nn);
-    if (slab_pass(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, a) < 0)
-      return cuda_fail(cudaGetLastError(), "stencil pass");
-    c->launches++;
+    if (pass > 0 && l) {   // the previous pass's halos before this pass's boundary planes
+      const cudaError_t e = cudaStreamWaitEvent(c->stream, d->hin, 0);
+      if (e != cudaSuccess) return cuda_fail(e, "wait halo");
+    }
+    const int k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, a,
+                                       overlap, reserve, d->bdone);
+    if (k < 0) return cuda_fail(cudaGetLastError(), "stencil pass");
+    c->launches += k;
     it += step;
     if (!l) continue;
+    // halo exchange on the exchange stream once the boundary planes are written
+    cudaError_t e = cudaStreamWaitEvent(d->xs, d->bdone, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "wait boundary");
     float* out = pass_buffer(c, pass + 1);
     ncclResult_t r = l->GroupStart();
     if (d->rank > 0) {
       if (r == ncclSuccess)
-        r = l->Send(plane_ptr(c, out, c->li_lo), count, ncclFloat32, d->rank - 1, d->comm,
-                    c->stream);
+        r = l->Send(plane_ptr(c, out, c->li_lo), count, ncclFloat32, d->rank - 1, d->comm, d->xs);
       if (r == ncclSuccess)
-        r = l->Recv(plane_ptr(c, out, c->li_lo - kHalo), count, ncclFloat32, d->rank - 1,
-                    d->comm, c->stream);
+        r = l->Recv(plane_ptr(c, out, c->li_lo - kHalo), count, ncclFloat32, d->rank - 1, d->comm,
+                    d->xs);
     }
     if (d->rank < d->nranks - 1) {
       if (r == ncclSuccess)
-        r = l->Send(plane_ptr(c, out, c->li_hi - kHalo), count, ncclFloat32, d->rank + 1,
-                    d->comm, c->stream);
+        r = l->Send(plane_ptr(c, out, c->li_hi - kHalo), count, ncclFloat32, d->rank + 1, d->comm,
+                    d->xs);
       if (r == ncclSuccess)
-        r = l->Recv(plane_ptr(c, out, c->li_hi), count, ncclFloat32, d->rank + 1, d->comm,
-                    c->stream);
+        r = l->Recv(plane_ptr(c, out, c->li_hi), count, ncclFloat32, d->rank + 1, d->comm, d->xs);
     }
     const ncclResult_t r2 = l->GroupEnd();
     if (r != ncclSuccess) return nccl_fail(r, "halo exchange");
     if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+    if ((e = cudaEventRecord(d->hin, d->xs)) != cudaSuccess) return cuda_fail(e, "halo event");
+  }
+  if (l && pass > 0) {
+    const cudaError_t e = cudaStreamWaitEvent(c->stream, d->hin, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "wait halo");
   }
   if (time_loop_finish(c, pass_buffer(c, pass), a) < 0) return cuda_fail(cudaGetLastError(), "end");
   if (l && nn > 0) {

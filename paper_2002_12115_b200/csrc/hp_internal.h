@@ -111,6 +111,12 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
 // two Jacobi iterations per pass (temporal blocking); 0 = not applicable
 int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
                        const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms);
+// one two-step pass of a slab in two parts (halo exchange overlapped with the
+// interior): part 1 = boundary plane pairs, part 2 = interior on <= sms - reserve
+// CTAs; 0 = slab too thin
+int launch_stencil_tb2_part(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                            const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms,
+                            int part, int reserve);
 // `passes` >= 2 two-step passes in ONE launch (units of pass t+1 start as soon as
 // their neighbourhood in pass t is done); result in p_out if passes is odd, else
 // p_in; 0 = not applicable (caller launches pass by pass)

@@ -108,15 +108,27 @@ struct Unit {           // one contiguous run of planes of one tile
 // the same planes at the same time, so the halo rows a tile shares with its
 // neighbours are served from L2, and a whole column pays no chunk boundary
 // (the two extra planes a unit loads and computes).
+// Two-range mode (r2_hi > r2_lo, two-step kernel only): exactly two plane ranges per
+// tile, [0, ni) and [r2_lo, r2_hi) relative to i_lo -- a slab's two boundary plane
+// pairs in one launch (decomp.cpp, halo exchange overlapped with the interior).
 struct Units {
   int ni, ktiles, tiles, len, full;
   uint32_t count;
-  __device__ Units(int ni_, int ktiles_, int tiles_, int len_, int full_)
-      : ni(ni_), ktiles(ktiles_), tiles(tiles_), len(len_), full(full_),
-        count((uint32_t)(full_ + (tiles_ - full_) * ((ni_ + len_ - 1) / len_))) {}
+  int r2_lo, r2_hi;
+  __device__ Units(int ni_, int ktiles_, int tiles_, int len_, int full_, int r2_lo_ = 0,
+                   int r2_hi_ = 0)
+      : ni(ni_), ktiles(ktiles_), tiles(tiles_), len(len_), full(r2_hi_ > r2_lo_ ? 0 : full_),
+        count(r2_hi_ > r2_lo_ ? (uint32_t)(2 * tiles_)
+                              : (uint32_t)(full_ + (tiles_ - full_) * ((ni_ + len_ - 1) / len_))),
+        r2_lo(r2_lo_), r2_hi(r2_hi_) {}
   __device__ void decode(uint32_t u, Unit& s) const {
     int t, c;
-    if (u < (uint32_t)full) {
+    if (r2_hi > r2_lo) {
+      t = (int)(u % (uint32_t)tiles);
+      c = (int)(u / (uint32_t)tiles);
+      s.ia = c ? r2_lo : 0;
+      s.ib = c ? r2_hi : ni;
+    } else if (u < (uint32_t)full) {
       t = (int)u;
       s.ia = 0;
       s.ib = ni;
@@ -655,7 +667,7 @@ template <int LW, int NW1_, int SC_, bool ST_ = false>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i_hi, int j_lo,
               int j_hi, int k_lo, int k_hi, int k_org, int ktiles, int chunk, int full, int g_lo,
-              int g_hi, float omega, GosaSink g, int reset, Flow fl) {
+              int g_hi, float omega, GosaSink g, int reset, Flow fl, int i_lo2, int i_hi2) {
   using T = Tb2<LW, NW1_, SC_>;
   constexpr int RPW = T::RPW, NW1 = T::NW1, NW2 = T::NW2, R1 = T::R1, TJ2 = T::TJ2,
                 QK = T::QK, TK2 = T::TK2, SC = T::SC;
@@ -680,7 +692,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const Units units(ni, ktiles, ktiles * jtiles, chunk, full);
+  const Units units(ni, ktiles, ktiles * jtiles, chunk, full, i_lo2 - i_lo, i_hi2 - i_lo);
   const uint32_t nunits = units.count * (uint32_t)fl.passes;   // queue: pass-major
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
@@ -1349,18 +1361,27 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
   return best;
 }
 
+struct Range2 {
+  int lo = 0, hi = 0;   // second output plane range (two-range launch), empty if hi <= lo
+  int grid_cap = 0;     // > 0: at most this many CTAs (SMs left to a concurrent kernel)
+};
+
 template <int LW, int NW1, int SC, bool ST = false>
 static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo, int i_hi,
                       int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
-                      int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
+                      int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms,
+                      const Range2& r2 = Range2{}) {
   using T = Tb2<LW, NW1, SC>;
   const int k_org = tb2_k_org();
   const int ktiles = (k_hi - k_org + T::TK2 - 1) / T::TK2;
   const int jtiles = (j_hi - j_lo + T::TJ2 - 1) / T::TJ2;
   const long long tiles = (long long)ktiles * jtiles;
   if (full < 0 || full > tiles) full = 0;
-  const long long units = full + (tiles - full) * ((i_hi - i_lo + chunk - 1) / chunk);
+  const bool two = r2.hi > r2.lo;
+  const long long units =
+      two ? 2 * tiles : full + (tiles - full) * ((i_hi - i_lo + chunk - 1) / chunk);
   long long grid = sms;
+  if (r2.grid_cap > 0 && grid > r2.grid_cap) grid = r2.grid_cap;
   if (grid > units * fl.passes) grid = units * fl.passes;
   if (units > g.capacity) return -1;   // one gosa partial per unit (of the last pass)
   fl.upp = (int)units;
@@ -1380,7 +1401,8 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo
   cfg.numAttrs = pdl ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC, ST>, maps, F, i_lo,
                                            i_hi, j_lo, j_hi, k_lo, k_hi, k_org, ktiles, chunk, full,
-                                           g_lo, g_hi, a.omega, g, a.gosa_reset, fl);
+                                           g_lo, g_hi, a.omega, g, a.gosa_reset, fl,
+                                           two ? r2.lo : 0, two ? r2.hi : 0);
   return e == cudaSuccess ? 1 : -1;
 }
 
@@ -1512,7 +1534,7 @@ int tx_error(const void* h) {
 // even one.  Returns 1, 0 (not applicable: the caller runs single steps), or -1.
 static int launch_two_step(const DevFields& F, const void* h, const float* p_in, float* p_out,
                            int passes, const LaunchArgs& a, const GosaSink& g, cudaStream_t s,
-                           int sms) {
+                           int sms, const Range2& r2 = Range2{}) {
   TmaState* t = const_cast<TmaState*>(static_cast<const TmaState*>(h));
   if (!t || (p_in != t->p && p_in != t->scratch) || passes < 1) return 0;
   const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
@@ -1526,7 +1548,7 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
   if (passes > 1 && !t->done) return 0;
   // the exchange kernel (one pass per launch) when enabled and its tiles can all
   // be resident
-  if (passes == 1) {
+  if (passes == 1 && r2.hi <= r2.lo && r2.grid_cap == 0) {
     const int r = launch_tx(t, F, p_in, p_out, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, a, g,
                             s, sms);
     if (r != 0) {
@@ -1566,12 +1588,12 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
   }
 #define HP_TB2(LW, NW1, SC) \
   launch_tb2<LW, NW1, SC>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo, g_hi, c.chunk, \
-                          c.full, a, g, s, sms)
+                          c.full, a, g, s, sms, r2)
   switch (v) {
     case 1:
       if (env_int("HIMENO_TB2_STASH") != 0)
         return launch_tb2<16, 8, 4, true>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo,
-                                          g_hi, c.chunk, c.full, a, g, s, sms);
+                                          g_hi, c.chunk, c.full, a, g, s, sms, r2);
       return HP_TB2(16, 8, 4);
     case 2: return HP_TB2(16, 6, 5);
     case 3: return HP_TB2(16, 5, 6);
@@ -1585,6 +1607,30 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
 int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, float* p_out,
                        const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms) {
   return launch_two_step(F, h, p_in, p_out, 1, a, g, s, sms);
+}
+
+// One two-step pass of a slab in parts (decomp.cpp): part 1 = the two boundary plane
+// pairs [li_lo, li_lo+2) and [li_hi-2, li_hi) in one launch (what the neighbours need;
+// gosa stored), part 2 = the interior [li_lo+2, li_hi-2) on at most sms - reserve CTAs
+// (gosa accumulated).  Same arithmetic per point as the whole pass: bit-identical.
+// Returns 1, 0 (slab too thin: run the whole pass), or -1.
+int launch_stencil_tb2_part(const DevFields& F, const void* h, const float* p_in, float* p_out,
+                            const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms,
+                            int part, int reserve) {
+  if (a.li_hi - a.li_lo < 6) return 0;
+  LaunchArgs b = a;
+  Range2 r2;
+  if (part == 1) {
+    b.li_hi = a.li_lo + 2;
+    r2.lo = a.li_hi - 2;
+    r2.hi = a.li_hi;
+  } else {
+    b.li_lo = a.li_lo + 2;
+    b.li_hi = a.li_hi - 2;
+    b.gosa_reset = 0;
+    r2.grid_cap = reserve > 0 ? std::max(1, sms - reserve) : sms;
+  }
+  return launch_two_step(F, h, p_in, p_out, 1, b, g, s, sms, r2);
 }
 
 // Flow launches pay where the per-pass drain matters: when one pass's tiles fit in

@@ -129,11 +129,15 @@ def test_halo_plan_is_symmetric():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [0, 1])
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("ranks", [1, 2, 3, 4])
 @pytest.mark.parametrize("name,nn", [("XS", 3), ("XS", 4), ("M", 2), ("M", 5)])
-def test_gpu_group_slabs_match_oracle(gpu, ranks, name, nn, tb):
-    """Virtual ranks on one GPU, one- and two-step passes: bit-exact with the full grid."""
+def test_gpu_group_slabs_match_oracle(gpu, monkeypatch, ranks, name, nn, tb, overlap):
+    """Virtual ranks on one GPU, one- and two-step passes, halo exchange after each whole
+    pass or overlapped with the interior (boundary planes first): bit-exact with the full
+    grid."""
+    monkeypatch.setenv("HIMENO_DD_OVERLAP", str(overlap))
     sz = himeno.size(name)
     ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
     lib = N.load()

@@ -509,12 +509,16 @@ def l_oracle_n4():
     return {3: (p3, g3), 4: (f["p"].copy(), g4)}
 
 
+@pytest.mark.parametrize("overlap", [0, 1])
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("ranks", [2, 4, 8])
-def test_l_grid_slabs_bit_exact(gpu, l_oracle_n4, ranks, tb):
-    """BASELINE config 3's decomposition (L split into 2/4/8 slabs, halo exchange and
-    gosa sum after the passes) with virtual ranks on one GPU, against the full grid."""
+def test_l_grid_slabs_bit_exact(gpu, monkeypatch, l_oracle_n4, ranks, tb, overlap):
+    """BASELINE config 3's decomposition (L split into 2/4/8 slabs, halo exchange --
+    after each pass, or overlapped with the interior: boundary planes first, exchange on
+    a comm stream -- and gosa sum after the passes) with virtual ranks on one GPU,
+    against the full grid."""
     from paper_2002_12115_b200 import dd
+    monkeypatch.setenv("HIMENO_DD_OVERLAP", str(overlap))
     lib = N.load()
     old = lib.hp_set_temporal_blocking(tb)
     try:

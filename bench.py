@@ -275,19 +275,36 @@ def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: i
         setup_s = time.perf_counter() - t_setup
         done, executed = {}, []
         measure = ev.measure
+        import threading
+        lock = threading.Lock()
+        busy = {d: 0.0 for d in sorted(set(devices))}    # program-run seconds per GPU
+        runs = {d: 0 for d in busy}
 
         def timed_measure(g):
             m = measure(g)
-            done[tuple(g)] = time.perf_counter()
-            if ev.lowered(g).failure is None:
-                executed.append(g)
+            st = ev.stats.get(tuple(g)) if ev.lowered(g).failure is None else None
+            with lock:
+                done[tuple(g)] = time.perf_counter()
+                if st is not None:
+                    executed.append(g)
+                    if m.seconds:
+                        busy[st["device"]] += m.seconds
+                        runs[st["device"]] += 1
             return m
 
         ev.measure = timed_measure
+        try:
+            import psutil
+            psutil.cpu_percent(interval=None)
+        except ImportError:   # host-load figures are context only
+            psutil = None
+        cpu0 = os.times()
         t0 = time.perf_counter()
         res = ga.run_ga(ga.GAConfig(population=pop, generations=gens, rng_seed=seed),
                         ev.gene_length, ev)
         el = time.perf_counter() - t0
+        cpu1 = os.times()
+        sys_pct = psutil.cpu_percent(interval=None) if psutil else None
         ev.measure = measure
         best = res.best
         out = {"size": size_name, "nn": nn, "population": pop, "generations": gens,
@@ -299,7 +316,16 @@ def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: i
                "fresh_evals_per_s": res.evaluations / el, "gens_per_s": gens / el,
                "best_genome": ga.genome_str(best.genome), "best_time_s": best.time_s,
                "best_source": best.eval_source,
-               "time_to_best_s": (done[best.genome] - t0) if best.genome in done else None}
+               "time_to_best_s": (done[best.genome] - t0) if best.genome in done else None,
+               # per GPU: seconds of program runs (the fitness wall time of each executed
+               # evaluation) and their share of the GA's wall time
+               "per_gpu": {str(d): {"runs": runs[d], "busy_s": busy[d], "busy_frac": busy[d] / el}
+                           for d in busy},
+               # host: the process's CPU seconds over the GA (host loops of gene-0 nests,
+               # planning, launches) as mean busy cores, and the whole machine's load
+               "host": {"process_cpu_s": (cpu1.user - cpu0.user) + (cpu1.system - cpu0.system),
+                        "mean_busy_cores": ((cpu1.user - cpu0.user) + (cpu1.system - cpu0.system)) / el,
+                        "cores": os.cpu_count(), "system_cpu_pct": sys_pct}}
         opt = OPTIMUM.get((size_name, nn))
         if opt is not None and best.time_s < 1000:
             g = tuple(int(c) for c in opt)
@@ -423,6 +449,11 @@ def run_ours(args, world, rank, local):
 
     dist = None
     if world > 1:
+        # NCCL's communicator set-up lines (rank count, transports, NVLS) on stderr, so
+        # the run's log shows the nranks the halo exchange and gosa all-reduce used;
+        # INIT only (no per-call logging inside the timed region)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -1480,6 +1480,7 @@ static int launch_tx(TmaState* t, const DevFields& F, const float* p_in, float* 
   if (env_int("HIMENO_TX_XRX") > 0) x.xrx = std::min(XRX, env_int("HIMENO_TX_XRX"));
   if (x.xrx < 10 + 2 * x.ahead || (x.xrx & (x.xrx - 1))) x.xrx = XRX;
   x.evl = env_int("HIMENO_TX_EVL") != 0 ? 1 : 0;   // evict_last: default (10% faster)
+  x.sleep_ns = env_int("HIMENO_TX_SLEEP") >= 0 ? env_int("HIMENO_TX_SLEEP") : 0;
   std::lock_guard<std::mutex> lock(g_tx_mu);
   if (++t->epoch >= (1u << 20)) {   // tags epoch * 4096 + plane stay in 32 bits
     if (cudaMemsetAsync(t->xr, 0, t->nxr * 8, s) != cudaSuccess ||

@@ -44,7 +44,7 @@ constexpr int XK = 128;        // owned columns per tile: 32 lanes x float4
 constexpr int XW = XK + 8;     // tile row stride: column c <-> k = k0 - 4 + c
 constexpr int XSP = 3;         // p0 ring slots
 constexpr int XSC = 4;         // coefficient stages
-constexpr int XSQ = 6;         // p1 ring slots
+constexpr int XSQ = 8;         // p1 ring slots
 constexpr int XNS = 5;         // TMEM stash slots per step-2 warp (48 columns each)
 // Global exchange ring depth.  A tile writes plane q's words only after its own
 // gather of plane q-8 (its coefficient stage q waits for the step-2 stash of plane
@@ -89,6 +89,7 @@ struct XBuf {
   unsigned epoch;
   int xrw, xcw, chunks;
   int ahead;          // stash up to this many planes ahead (1 .. XNS - 2)
+  int sleep_ns;       // exchange warp back-off between reloads of a plane's halo
   int xrx;            // ring depth in planes (power of two, <= XRX, >= 10 + 2 * ahead)
   int evl;            // 1: exchange words stored with an L2 evict_last policy
   int dbg;            // HIMENO_TX_DBG (experiments only): 1 = do not wait for the tags,
@@ -516,6 +517,9 @@ k_stencil_tx(const __grid_constant__ TxMaps maps, DevFields F, float* __restrict
           ++q;
         }
       } else {
+        // not published yet: back off before reloading (a tight retry loop takes
+        // issue slots from the stencil warps of this sub-partition)
+        if (x.sleep_ns > 0) __nanosleep((unsigned)x.sleep_ns);
         const uint64_t now = global_ns();
         if (t0 == 0) {
           t0 = now;

@@ -28,3 +28,23 @@ with B200Evaluator("XXS", nn=2, kinds={l: DirectiveKind.PARALLEL_LOOP_VECTOR for
 from paper_2002_12115_b200 import dd  # noqa: E402
 with dd.GroupJacobi("XS", [0, 0, 0]) as g:
     print("group", g.jacobi(2))
+# round 2: the flow launch (3 two-step passes in one launch), the overlapped halo
+# exchange (boundary launch + interior launch + comm-stream copies), and -- when
+# SANITIZE_TX=1 -- the tile-exchange kernel
+import os  # noqa: E402
+os.environ["HIMENO_TB2_FLOW"] = "1"
+os.environ["HIMENO_FLOW_CHUNK"] = "8"
+with N.Context(0, sz.I, sz.J, sz.K) as c:
+    c.init_device()
+    c.jacobi_device(6, 1)
+    print("flow", N.last_two_step_kernel(), c.read_gosa(1))
+del os.environ["HIMENO_TB2_FLOW"], os.environ["HIMENO_FLOW_CHUNK"]
+os.environ["HIMENO_DD_OVERLAP"] = "1"
+with dd.GroupJacobi("XS", [0, 0, 0]) as g:
+    print("group overlapped", g.jacobi(4))
+if os.environ.get("SANITIZE_TX") == "1":
+    os.environ["HIMENO_TX"] = "2"
+    with N.Context(0, sz.I, sz.J, sz.K) as c:
+        c.init_device()
+        c.jacobi_device(4, 1)
+        print("tx", N.last_two_step_kernel(), c.read_gosa(1), c.tx_status())

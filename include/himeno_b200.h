@@ -118,6 +118,9 @@ enum hp_flags {
   HP_FLAG_KERNEL_TIMING = 8,    /* CUDA events around every launch (slower)         */
   HP_FLAG_GRAPH_TIME_LOOP = 16, /* replay the device time loop as a CUDA graph      */
   HP_FLAG_FUSED_TIME_LOOP = 32, /* time loop: fused stencil with p/wrk2 rotation    */
+  HP_FLAG_HOST_REFERENCE = 128, /* genes = 0: the reference-faithful host build
+                                   (the program's loops, gcc -O2) instead of the
+                                   tuned one (-O3 -march=x86-64-v3); same values     */
   HP_FLAG_LITERAL_GOSA = 64     /* verification: when the last iteration's stencil
                                    runs on the device, its ss*ss terms are also
                                    written out (side kernel on the same device

@@ -5,7 +5,8 @@
 * kernels.cu   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
                --fmad=false (bit-exact with the host loops / oracle)
 * executor.cpp g++ -O3 -march=x86-64-v3 -ffp-contract=off (AVX2 host loops, no FMA
-  contraction: every product and sum rounds separately, as on the device)
+  contraction: every product and sum rounds separately, as on the device);
+  host_loops_ref.cpp g++ -O2 (the reference's compile template, HP_FLAG_HOST_REFERENCE)
 * link         nvcc -shared -cudart static  ->  paper_2002_12115_b200/_native/
 
 Generated executors (codegen.py; generic.APPS): for every application text with a
@@ -123,7 +124,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cpp")):
         obj = OUT_DIR / (src.stem + ".o")
-        _run(["g++", "-O3", "-march=x86-64-v3", "-std=c++17", "-fPIC", "-ffp-contract=off",
+        # *_ref.cpp: the reference's compile template (`gcc -O2 -w`, evaluators.py:154-165):
+        # the reference-faithful host build of the loops (HP_FLAG_HOST_REFERENCE)
+        opt = ["-O2"] if src.stem.endswith("_ref") else ["-O3", "-march=x86-64-v3"]
+        _run(["g++", *opt, "-std=c++17", "-fPIC", "-ffp-contract=off",
               "-fno-fast-math",
               "-Wall", "-Wno-unused-function", "-I", str(cuda / "include"), *inc,
               "-c", str(src), "-o", str(obj)], verbose)

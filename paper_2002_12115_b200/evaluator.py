@@ -60,6 +60,11 @@ class MeasuredTime:
 
 
 TRANSFER_MODES = ("batched", "per-loop")
+# genes = 0 run the library's host loops: "tuned" (g++ -O3 -march=x86-64-v3, the
+# program as a tuned application) or "reference" (the program's literal loops built
+# like the reference's compile template, gcc -O2: host-heavy patterns cost what the
+# reference's binary makes them cost).  Same values either way.
+HOST_BUILDS = ("tuned", "reference")
 
 
 def _size_from_refs(refs):
@@ -79,13 +84,16 @@ class B200Evaluator:
                  nested_policy: str = "reject", coherence_guard: bool = True,
                  fused_time_loop: bool = True, fresh_process: bool = True,
                  poison_device: bool = False, timeout_s: float = 180.0,
-                 workers_per_device: int = 1):
+                 workers_per_device: int = 1, host_build: str = "tuned"):
         if transfer_mode not in TRANSFER_MODES:
             raise ConfigError(f"transfer_mode must be one of {TRANSFER_MODES}")
         if nested_policy not in NESTED_POLICIES:
             raise ConfigError(f"nested_policy must be one of {NESTED_POLICIES}")
         if nn < 1:
             raise ConfigError("nn must be >= 1")
+        if host_build not in HOST_BUILDS:
+            raise ConfigError(f"host_build must be one of {HOST_BUILDS}")
+        self.host_build = host_build
         prog = himeno.program()
         self.loops = loops if loops is not None else prog.model.loops
         self.refs = refs if refs is not None else prog.model.refs
@@ -99,7 +107,8 @@ class B200Evaluator:
         self.flags = ((N.FLAG_COHERENCE_GUARD if coherence_guard else 0)
                       | (N.FLAG_FUSED_TIME_LOOP if fused_time_loop else 0)
                       | (N.FLAG_FRESH_PROCESS if fresh_process else 0)
-                      | (N.FLAG_POISON_DEVICE if poison_device else 0))
+                      | (N.FLAG_POISON_DEVICE if poison_device else 0)
+                      | (N.FLAG_HOST_REFERENCE if host_build == "reference" else 0))
         N.load()   # fail loudly now: no CPU fallback exists
         if devices is None:
             devices = [0]

@@ -38,6 +38,7 @@ FLAG_KERNEL_TIMING = 8
 FLAG_GRAPH_TIME_LOOP = 16
 FLAG_FUSED_TIME_LOOP = 32
 FLAG_LITERAL_GOSA = 64
+FLAG_HOST_REFERENCE = 128
 MAX_SAMPLES = 8
 SLAB_HALO = 2      # halo planes per side of a slab context (csrc/decomp.cpp kHalo)
 

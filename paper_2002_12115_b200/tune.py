@@ -204,6 +204,9 @@ def main(argv=None) -> int:
     ap.add_argument("--workers-per-device", default="1",
                     help="concurrent evaluations per GPU, or 'auto' (host cores / GPUs)")
     ap.add_argument("--transfer-mode", default="batched", choices=["batched", "per-loop"])
+    ap.add_argument("--host-build", default="tuned", choices=["tuned", "reference"],
+                    help="genes = 0: the library's tuned host loops, or the program's loops "
+                         "built like the reference's compile template (gcc -O2)")
     ap.add_argument("--out")
     args = ap.parse_args(argv)
     devices = "all" if args.devices == "all" else [int(d) for d in args.devices.split(",")]
@@ -228,7 +231,7 @@ def main(argv=None) -> int:
         return 0 if ok else 3
     with B200Evaluator(args.size, nn=args.nn, devices=devices,
                        workers_per_device=workers,
-                       transfer_mode=args.transfer_mode) as ev:
+                       transfer_mode=args.transfer_mode, host_build=args.host_build) as ev:
         _report, ok = run_tuning(ev, cfg, args.out)
     return 0 if ok else 3
 

@@ -636,3 +636,29 @@ def test_flow_launch_is_the_default_on_M(gpu):
         ctx.init_device()
         ctx.jacobi_device(8, 1)
         assert N.last_two_step_kernel() == "k_stencil_tb2 (flow)"
+
+
+# --- reference-faithful host build of the gene-0 loops ---------------------------------
+
+@pytest.mark.parametrize("name", ["XS", "M"])
+def test_host_reference_build_same_values(gpu, name):
+    """host_build="reference" (the program's literal loops, g++ -O2 like the reference's
+    compile template) computes exactly what the tuned host build does, for the all-CPU
+    program and for mixed patterns; only its speed differs."""
+    sz = himeno.size(name)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, 3)
+    times = {}
+    for build in ("tuned", "reference"):
+        with B200Evaluator(name, nn=3, host_build=build) as ev:
+            for g in ("0" * 13, "0000000100100", "1001000000000", "0000001000000"):
+                genome = tuple(int(c) for c in g)
+                res = ev.run(genome)
+                p = ev.read_field("p", side=0)
+                assert np.array_equal(p, ref["fields"]["p"]), (build, g)
+                assert abs(res.gosa - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"], (build, g)
+                if g == "0" * 13:
+                    # the all-CPU program's printed float gosa: the literal fp32 sum
+                    assert np.float32(res.gosa_f32) == np.float32(ref["gosa32"]), build
+            times[build] = min(ev.measure((0,) * 13).seconds for _ in range(3))
+    print(f"{name} all-CPU program: tuned {times['tuned'] * 1e3:.2f} ms, "
+          f"reference build {times['reference'] * 1e3:.2f} ms")

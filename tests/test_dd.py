@@ -44,7 +44,17 @@ def stencil_slab(f, lo, hi, jmax, kmax, omega=F32(0.8)):
     return out, float(np.sum((ss * ss).astype(np.float64)))
 
 
-def _rank_main(rank, world, name, nn, port, q):
+def stencil_into(out, f, lo, hi, jmax, kmax, omega=F32(0.8)):
+    """stencil_slab for planes [lo, hi) written into `out` (the overlapped schedule
+    computes a slab's boundary planes and its interior in two calls)."""
+    if hi <= lo:
+        return 0.0
+    new, part = stencil_slab(f, lo, hi, jmax, kmax, omega)
+    out[lo:hi] = new[lo:hi]
+    return part
+
+
+def _rank_main(rank, world, name, nn, port, q, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sz = himeno.size(name)
@@ -63,16 +73,34 @@ def _rank_main(rank, world, name, nn, port, q):
     n = e - b
     gosa = 0.0
     for _ in range(nn):
-        f["p"], part = stencil_slab(f, H, n + H, sz.J - 1, sz.K - 1)
         sends, recvs = plan[rank]
-        reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(f["p"][pl:pl + H])), dst)
-                for dst, pl in sends]
-        for src, pl in recvs:
-            buf = torch.empty(f["p"][pl:pl + H].shape, dtype=torch.float32)
-            dist.recv(buf, src)
-            f["p"][pl:pl + H] = buf.numpy()
-        for r in reqs:
-            r.wait()
+        if overlap and n >= 2 * H + 2:
+            # hp_dd_jacobi's overlapped pass: the planes the neighbours need first,
+            # their exchange in flight while the interior is computed, then the wait
+            out = f["p"].copy()
+            part = stencil_into(out, f, H, H + H, sz.J - 1, sz.K - 1)
+            part += stencil_into(out, f, n, n + H, sz.J - 1, sz.K - 1)
+            reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(out[pl:pl + H])), dst)
+                    for dst, pl in sends]
+            bufs = [(torch.empty(out[pl:pl + H].shape, dtype=torch.float32), src, pl)
+                    for src, pl in recvs]
+            reqs += [dist.irecv(buf, src) for buf, src, _ in bufs]
+            part += stencil_into(out, f, H + H, n, sz.J - 1, sz.K - 1)   # the interior
+            for r in reqs:
+                r.wait()
+            for buf, _, pl in bufs:
+                out[pl:pl + H] = buf.numpy()
+            f["p"] = out
+        else:
+            f["p"], part = stencil_slab(f, H, n + H, sz.J - 1, sz.K - 1)
+            reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(f["p"][pl:pl + H])), dst)
+                    for dst, pl in sends]
+            for src, pl in recvs:
+                buf = torch.empty(f["p"][pl:pl + H].shape, dtype=torch.float32)
+                dist.recv(buf, src)
+                f["p"][pl:pl + H] = buf.numpy()
+            for r in reqs:
+                r.wait()
         t = torch.tensor([part], dtype=torch.float64)
         dist.all_reduce(t)
         gosa = float(t.item())
@@ -87,13 +115,17 @@ def _rank_main(rank, world, name, nn, port, q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_gloo_slab_decomposition_matches_oracle(world):
-    """Host slabs with HALO-deep halos, exchanged per dd.halo_plan after every step."""
+def test_gloo_slab_decomposition_matches_oracle(world, overlap):
+    """Host slabs with HALO-deep halos, exchanged per dd.halo_plan after every step --
+    or, as hp_dd_jacobi overlaps it, boundary planes first, the exchange in flight
+    (isend/irecv) while the interior is computed."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + world * 7 + os.getpid() % 1000
-    procs = [ctx.Process(target=_rank_main, args=(r, world, "XXS", 3, port, q))
+    port = 29500 + world * 7 + int(overlap) * 3 + os.getpid() % 1000
+    name = "XS" if overlap else "XXS"    # XS slabs are deep enough to split
+    procs = [ctx.Process(target=_rank_main, args=(r, world, name, 3, port, q, overlap))
              for r in range(world)]
     for p in procs:
         p.start()

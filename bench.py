@@ -318,7 +318,8 @@ def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: i
                "best_source": best.eval_source,
                "time_to_best_s": (done[best.genome] - t0) if best.genome in done else None,
                # per GPU: seconds of program runs (the fitness wall time of each executed
-               # evaluation) and their share of the GA's wall time
+               # evaluation) summed over its worker slots, and that sum over the GA's wall
+               # time (concurrent slots overlap, so it can exceed 1)
                "per_gpu": {str(d): {"runs": runs[d], "busy_s": busy[d], "busy_frac": busy[d] / el}
                            for d in busy},
                # host: the process's CPU seconds over the GA (host loops of gene-0 nests,

@@ -662,3 +662,46 @@ def test_host_reference_build_same_values(gpu, name):
             times[build] = min(ev.measure((0,) * 13).seconds for _ in range(3))
     print(f"{name} all-CPU program: tuned {times['tuned'] * 1e3:.2f} ms, "
           f"reference build {times['reference'] * 1e3:.2f} ms")
+
+
+# --- the new launch modes under concurrent contexts on one GPU --------------------------
+
+@pytest.mark.parametrize("mode", ["flow", "tx"])
+def test_concurrent_contexts_new_launch_modes(gpu, monkeypatch, mode):
+    """Worker slots share a GPU (the GA's population sharding with several contexts per
+    device): four contexts run the device time loop at once -- as multi-pass flow launches
+    (CTAs wait only on units claimed earlier in their own launch), or with the tile-exchange
+    kernel (its launches are chained per device across streams, so two never hold SMs the
+    other needs).  Every context's field equals the oracle's; no neighbour-wait timeout."""
+    from concurrent.futures import ThreadPoolExecutor
+    nn = 8
+    if mode == "flow":
+        monkeypatch.setenv("HIMENO_TB2_FLOW", "1")
+        sz = himeno.size("XS")
+    else:
+        monkeypatch.setenv("HIMENO_TX", "2")
+        monkeypatch.setenv("HIMENO_TX_MINCHUNK", "4")
+        sz = himeno.custom_size(37, 21, 70)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(1)
+    ctxs = [N.Context(0, sz.I, sz.J, sz.K) for _ in range(4)]
+    try:
+        def one(c):
+            out = []
+            for _ in range(3):
+                c.init_device()
+                c.jacobi_device(nn, 1)
+                out.append((c.read_field("p", 1), c.read_gosa(1), c.tx_status()))
+            return out
+        with ThreadPoolExecutor(max_workers=4) as pool:
+            results = list(pool.map(one, ctxs))
+    finally:
+        for c in ctxs:
+            c.close()
+        lib.hp_set_temporal_blocking(old)
+    for runs in results:
+        for p, g, st in runs:
+            assert st == 0
+            assert np.array_equal(p, ref["fields"]["p"])
+            assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]

@@ -732,7 +732,6 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         // lane l: neighbour tile l / 3 of the 3 x 3 block, l % 3-th plane chunk
         // overlapping [ia-2, ib+2) (planes the step-1 box reads, and the planes this
         // unit overwrites in the buffer the previous pass read)
-        bool ok = true;
         const int d = lane / 3, co = lane % 3;
         if (d < 9) {
           const int jn = s.jt + d / 3 - 1, kn = s.kt + d % 3 - 1;
@@ -756,7 +755,6 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
             }
           }
         }
-        (void)ok;
         __syncwarp();
         // the previous pass's generic-proxy stores before this CTA's TMA (async
         // proxy) reads of them

@@ -207,6 +207,9 @@ def main(argv=None) -> int:
     ap.add_argument("--host-build", default="tuned", choices=["tuned", "reference"],
                     help="genes = 0: the library's tuned host loops, or the program's loops "
                          "built like the reference's compile template (gcc -O2)")
+    ap.add_argument("--checkpoint", default=None,
+                    help="JSONL of every fresh measurement (with its metrics); rerun with the "
+                         "same file to resume an interrupted search (checkpoint.py)")
     ap.add_argument("--out")
     args = ap.parse_args(argv)
     devices = "all" if args.devices == "all" else [int(d) for d in args.devices.split(",")]
@@ -232,7 +235,14 @@ def main(argv=None) -> int:
     with B200Evaluator(args.size, nn=args.nn, devices=devices,
                        workers_per_device=workers,
                        transfer_mode=args.transfer_mode, host_build=args.host_build) as ev:
-        _report, ok = run_tuning(ev, cfg, args.out)
+        plugin = ev
+        if args.checkpoint:
+            from .checkpoint import CheckpointedEvaluator
+            plugin = CheckpointedEvaluator(ev, args.checkpoint)
+        _report, ok = run_tuning(plugin, cfg, args.out)
+        if args.checkpoint:
+            print(f"checkpoint {args.checkpoint}: {plugin.measured} measured, "
+                  f"{plugin.replayed} replayed")
     return 0 if ok else 3
 
 

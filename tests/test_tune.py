@@ -40,3 +40,25 @@ def test_tuning_run_end_to_end(gpu, tmp_path):
     assert len((tmp_path / "generations.jsonl").read_text().splitlines()) == 4
     assert set(json.loads((tmp_path / "report.json").read_text())) >= {
         "baseline_time_s", "best_time_s", "improvement_ratio", "best_genome", "plan", "verification"}
+
+
+@pytest.mark.gpu
+def test_tuning_checkpoint_resume_on_the_b200(gpu, tmp_path):
+    """tune --checkpoint: the first run records every fresh measurement with its metrics
+    (device, bytes moved, launches, PCIe rate); a second run with the same file replays
+    them all (no program runs) and reports the same best genome."""
+    from paper_2002_12115_b200 import tune
+    ck = tmp_path / "evals.jsonl"
+    args = ["--size", "XS", "--nn", "3", "--population", "8", "--generations", "3",
+            "--checkpoint", str(ck)]
+    assert tune.main(args + ["--out", str(tmp_path / "a")]) == 0
+    recs = [json.loads(l) for l in ck.read_text().splitlines()]
+    assert recs and all("genome" in r and "outcome" in r for r in recs)
+    ran = [r for r in recs if r["outcome"] == "ok"]
+    assert ran and all(r["metrics"]["device"] == 0 and r["metrics"]["n_launch"] >= 0 for r in ran)
+    n_lines = len(recs)
+    assert tune.main(args + ["--out", str(tmp_path / "b")]) == 0
+    assert len(ck.read_text().splitlines()) == n_lines        # nothing new was measured
+    a = json.loads((tmp_path / "a" / "report.json").read_text())
+    b = json.loads((tmp_path / "b" / "report.json").read_text())
+    assert a["best_genome"] == b["best_genome"] and a["best_time_s"] == b["best_time_s"]

@@ -116,7 +116,10 @@ enum hp_flags {
   HP_FLAG_FRESH_PROCESS = 2,    /* reset host arrays to static-zero before the run  */
   HP_FLAG_POISON_DEVICE = 4,    /* fill device mirrors with NaN before the run      */
   HP_FLAG_KERNEL_TIMING = 8,    /* CUDA events around every launch (slower)         */
-  HP_FLAG_GRAPH_TIME_LOOP = 16, /* replay the device time loop as a CUDA graph      */
+  HP_FLAG_GRAPH_TIME_LOOP = 16, /* reserved, no effect: the time loop's passes are
+                                   enqueued back to back with programmatic dependent
+                                   launch, or as one flow launch (a captured graph
+                                   would replay a flow launch's completion tags)     */
   HP_FLAG_FUSED_TIME_LOOP = 32, /* time loop: fused stencil with p/wrk2 rotation    */
   HP_FLAG_HOST_REFERENCE = 128, /* genes = 0: the reference-faithful host build
                                    (the program's loops, gcc -O2) instead of the

@@ -53,10 +53,10 @@ class Replay:
         return MeasuredTime.ok(t)
 
 
-def measure_table(size: str, nn: int, reps: int) -> dict:
+def measure_table(size: str, nn: int, reps: int, host_build: str = "tuned") -> dict:
     from paper_2002_12115_b200.evaluator import B200Evaluator
     table = {}
-    with B200Evaluator(size, nn=nn) as ev:
+    with B200Evaluator(size, nn=nn, host_build=host_build) as ev:
         ev.measure((0,) * ev.gene_length)
         for g in valid_genomes(ev.loops, ev.eligible_ids):
             ts = [ev.measure(g).seconds for _ in range(reps)]
@@ -83,12 +83,13 @@ def replay_sweep(table: dict, gene_len: int = 13) -> list:
     return rows
 
 
-def live_sweep(table: dict, size: str, nn: int, workers: int) -> list:
+def live_sweep(table: dict, size: str, nn: int, workers: int, host_build: str = "tuned") -> list:
     from paper_2002_12115_b200.evaluator import B200Evaluator
     opt_g = min(table, key=table.get)
     rows = []
     for policy in ("reject", "outermost"):
-        with B200Evaluator(size, nn=nn, workers_per_device=workers, nested_policy=policy) as ev:
+        with B200Evaluator(size, nn=nn, workers_per_device=workers, nested_policy=policy,
+                           host_build=host_build) as ev:
             ev.prepare()
             ev.measure((0,) * ev.gene_length)
             for pop, gens in CONFIGS:
@@ -147,6 +148,8 @@ def main():
     ap.add_argument("--table", help="JSONL table (genome, time_s): skip phase A")
     ap.add_argument("--table-out", default=str(ROOT / "profiles" / "r02_evalall_M.jsonl"))
     ap.add_argument("--no-live", action="store_true")
+    ap.add_argument("--host-build", default="tuned", choices=["tuned", "reference"],
+                    help="gene-0 loops: tuned host build or the reference's gcc -O2 template")
     ap.add_argument("--out", default=str(ROOT / "profiles" / "r02_ga_vs_optimum.json"))
     a = ap.parse_args()
     if a.table:
@@ -156,15 +159,15 @@ def main():
             if "genome" in d and d.get("time_s"):
                 table[tuple(int(c) for c in d["genome"])] = d["time_s"]
     else:
-        table = measure_table(a.size, a.nn, a.reps)
+        table = measure_table(a.size, a.nn, a.reps, a.host_build)
         with open(a.table_out, "w") as fh:
             for g, t in sorted(table.items(), key=lambda kv: kv[1]):
                 fh.write(json.dumps({"genome": ga.genome_str(g), "time_s": t}) + "\n")
     opt_g = min(table, key=table.get)
     rows = replay_sweep(table)
     if not a.no_live:
-        rows += live_sweep(table, a.size, a.nn, a.workers)
-    doc = {"size": a.size, "nn": a.nn, "runnable_genomes": len(table),
+        rows += live_sweep(table, a.size, a.nn, a.workers, a.host_build)
+    doc = {"size": a.size, "nn": a.nn, "host_build": a.host_build, "runnable_genomes": len(table),
            "optimum": {"genome": ga.genome_str(opt_g), "time_s": table[opt_g]},
            "criterion": "best within 5 % of the optimum (SPEC.md:552)",
            "summary": summarize(rows), "runs": rows}

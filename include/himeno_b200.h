@@ -263,7 +263,8 @@ int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
 /* Diagnostics: the dynamic shared-memory limit (bytes) the large-shared-memory
  * kernel `id` has in `device`'s context (0..2 single-step stencil with 2..4
  * stages, 3..6 two-step shapes, 7 two-step with the tensor-memory stash, 8 the
- * two-step tile-exchange kernel).  The library raises it per device before the
+ * two-step tile-exchange kernel, 9 kernel 7 with evict_first coefficient loads, used
+ * by flow launches).  The library raises it per device before the
  * first launch there. */
 int hp_smem_optin(int id, int device, int* bytes);
 /* Diagnostics: the kernel the most recent two-step launch (any context) used:

@@ -118,8 +118,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     inc = ["-I", str(INCLUDE), "-I", str(CSRC)]
     for src in sorted(CSRC.glob("*.cu")):
         obj = OUT_DIR / (src.stem + ".o")
+        extra = os.environ.get("HP_EXTRA_NVCC_FLAGS", "").split()   # experiment builds only
         _run([nvcc, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *extra,
               *inc, "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cpp")):

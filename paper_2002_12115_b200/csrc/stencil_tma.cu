@@ -663,7 +663,12 @@ __device__ void unit_finish(const GosaSink& g, uint32_t u, uint32_t upp, const F
   }
 }
 
-template <int LW, int NW1_, int SC_, bool ST_ = false>
+// CPOL_ = 1: the coefficient TMA loads carry an L2 evict_first policy.  The flow launch
+// (several passes in flight, small grids) runs 2.7 % faster with it on M; on L, whose
+// step-1 halo lines must survive in L2 until the neighbouring tile reads them, it costs
+// 28 % (profiles/r02_flow.md), so per-pass launches keep CPOL_ = 0 (no hint at all: an
+// evict_normal hint already costs 0.7 %).
+template <int LW, int NW1_, int SC_, bool ST_ = false, int CPOL_ = 0>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i_hi, int j_lo,
               int j_hi, int k_lo, int k_hi, int k_org, int ktiles, int chunk, int full, int g_lo,
@@ -719,6 +724,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
     // ------------------------------------------------------------- producer
     // lane 0 claims units and issues the TMA loads; in a flow launch the whole warp
     // first waits for the unit's dependencies (one completion tag per lane)
+    uint64_t cpolicy = 0;
+    if constexpr (CPOL_ == 1)
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(cpolicy));
     uint32_t sp = 0, sc = 0;
     Unit s{0, 0, 0, 0};
     for (uint32_t n = 0;; ++n) {
@@ -778,9 +786,14 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
           const int slot = sc % SC;
           if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
           mbar_expect_tx(&cfull[slot], NCOEF * T::kCExtBytes);
-          for (int c = 0; c < NCOEF; ++c)
-            tma_load_3d(cring + slot * T::kCSlot + c * T::kCExtBytes, &maps.coef[c], &cfull[slot],
-                        k0 - 4, j0 - 1, m);
+          for (int c = 0; c < NCOEF; ++c) {
+            if constexpr (CPOL_ == 1)
+              tma_load_3d_hint(cring + slot * T::kCSlot + c * T::kCExtBytes, &maps.coef[c],
+                               &cfull[slot], k0 - 4, j0 - 1, m, cpolicy);
+            else
+              tma_load_3d(cring + slot * T::kCSlot + c * T::kCExtBytes, &maps.coef[c], &cfull[slot],
+                          k0 - 4, j0 - 1, m);
+          }
           ++sc;
         }
       }
@@ -1211,6 +1224,7 @@ const void* smem_kernel(int id) {
     case 6: return (const void*)k_stencil_tb2<16, 5, 6, false>;
     case 7: return (const void*)k_stencil_tb2<16, 8, 4, true>;
     case 8: return (const void*)k_stencil_tx<kTxTJ>;
+    case 9: return (const void*)k_stencil_tb2<16, 8, 4, true, 1>;
     default: return nullptr;
   }
 }
@@ -1364,7 +1378,7 @@ struct Range2 {
   int grid_cap = 0;     // > 0: at most this many CTAs (SMs left to a concurrent kernel)
 };
 
-template <int LW, int NW1, int SC, bool ST = false>
+template <int LW, int NW1, int SC, bool ST = false, int CPOL = 0>
 static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo, int i_hi,
                       int j_lo, int j_hi, int k_lo, int k_hi, int g_lo, int g_hi, int chunk,
                       int full, const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms,
@@ -1385,7 +1399,7 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo
   fl.upp = (int)units;
   const size_t smem = T::smem_bytes();
   // the work-queue counter is zero: set at context creation, reset by the last CTA
-  if (!ensure_smem_optin((const void*)k_stencil_tb2<LW, NW1, SC, ST>, (int)smem)) return -1;
+  if (!ensure_smem_optin((const void*)k_stencil_tb2<LW, NW1, SC, ST, CPOL>, (int)smem)) return -1;
   static const bool pdl = env_int("HIMENO_TB2_PDL") != 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute la[1];
@@ -1397,7 +1411,7 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo
   cfg.stream = s;
   cfg.attrs = la;
   cfg.numAttrs = pdl ? 1 : 0;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC, ST>, maps, F, i_lo,
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_stencil_tb2<LW, NW1, SC, ST, CPOL>, maps, F, i_lo,
                                            i_hi, j_lo, j_hi, k_lo, k_hi, k_org, ktiles, chunk, full,
                                            g_lo, g_hi, a.omega, g, a.gosa_reset, fl,
                                            two ? r2.lo : 0, two ? r2.hi : 0);
@@ -1590,9 +1604,13 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
                           c.full, a, g, s, sms, r2)
   switch (v) {
     case 1:
-      if (env_int("HIMENO_TB2_STASH") != 0)
+      if (env_int("HIMENO_TB2_STASH") != 0) {
+        if (passes > 1 && env_int("HIMENO_FLOW_CPOL") != 0)
+          return launch_tb2<16, 8, 4, true, 1>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                               g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
         return launch_tb2<16, 8, 4, true>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi, g_lo,
                                           g_hi, c.chunk, c.full, a, g, s, sms, r2);
+      }
       return HP_TB2(16, 8, 4);
     case 2: return HP_TB2(16, 6, 5);
     case 3: return HP_TB2(16, 5, 6);

@@ -1582,14 +1582,16 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
   fl.out[1] = const_cast<float*>(p_in);
   if (passes > 1) {
     // a unit of pass t+1 waits for whole neighbouring units of pass t: chunked units
-    // only (whole columns would make every wait a wait for the entire pass)
-    c.full = 0;
+    // only (whole columns would make every wait a wait for the entire pass), unless
+    // HIMENO_FLOW_MODEL=1 keeps the per-pass model's schedule (whole columns + tail)
+    const bool keep_model = env_int("HIMENO_FLOW_MODEL") > 0;
+    if (!keep_model) c.full = 0;
     // balanced chunks of about 22 planes (M, 126 planes: 6 x 21 -> 43.8 us per pass;
     // 16 -> 45.6, 22 -> 44.1, 24 -> 44.6, 32 -> 48.7; profiles/r02_flow.md)
     const int fc = env_int("HIMENO_FLOW_CHUNK");
     const int ni = i_hi - i_lo;
     const int nch = std::max(1, (ni + 11) / 22);
-    c.chunk = fc > 0 ? fc : (ni + nch - 1) / nch;
+    if (!keep_model) c.chunk = fc > 0 ? fc : (ni + nch - 1) / nch;
     fl.done = t->done;
     std::lock_guard<std::mutex> lock(g_tx_mu);
     if (++t->flow_epoch >= (1u << 20) - 1u) {   // tags epoch * 4096 + pass + 1 in 32 bits

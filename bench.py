@@ -259,7 +259,8 @@ OPTIMUM = {("M", 3): "1001001000000"}
 
 
 def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: int,
-                  workers: int = 1, nested_policy: str = "reject") -> dict:
+                  workers: int = 1, nested_policy: str = "reject",
+                  host_build: str = "tuned") -> dict:
     """run_ga with the B200 evaluator.  Counts what the reference's procedure would
     count as work: `executed_evals` are runs of the program; genomes with nested
     compute constructs are rejected before anything launches (the reference's
@@ -268,7 +269,7 @@ def ga_throughput(devices, size_name: str, nn: int, pop: int, gens: int, seed: i
     from paper_2002_12115_b200.evaluator import B200Evaluator
     devices = [devices] if isinstance(devices, int) else list(devices)
     with B200Evaluator(size_name, nn=nn, devices=devices, workers_per_device=workers,
-                       nested_policy=nested_policy) as ev:
+                       nested_policy=nested_policy, host_build=host_build) as ev:
         t_setup = time.perf_counter()
         ev.prepare()                                       # one device context per slot
         ev.measure((0,) * ev.gene_length)                  # first-touch warm-up

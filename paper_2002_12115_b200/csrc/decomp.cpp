@@ -24,6 +24,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -272,8 +273,12 @@ Nccl* nccl() {
   static bool tried = false;
   if (tried) return lib.handle ? &lib : nullptr;
   tried = true;
-  // prefer an NCCL the process already loaded (torch's), else the system one
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  // HIMENO_NCCL_LIB: an explicit library (tests: tests/nccl_shim.cpp runs the NCCL
+  // transport with virtual ranks on one GPU); else prefer an NCCL the process already
+  // loaded (torch's), else the system one
+  void* h = nullptr;
+  if (const char* e = getenv("HIMENO_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!h) return nullptr;

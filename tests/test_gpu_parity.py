@@ -705,3 +705,20 @@ def test_concurrent_contexts_new_launch_modes(gpu, monkeypatch, mode):
             assert st == 0
             assert np.array_equal(p, ref["fields"]["p"])
             assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+
+
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_xl_grid_8_slabs_bit_exact(gpu, monkeypatch, xl_oracle, overlap):
+    """BASELINE config 5's grid (XL 513x513x1025) decomposed into 8 slabs -- virtual ranks
+    on one GPU, halo exchange after each pass or overlapped with the interior -- against
+    the full-grid oracle at nn = 2 and 4."""
+    from paper_2002_12115_b200 import dd
+    monkeypatch.setenv("HIMENO_DD_OVERLAP", str(overlap))
+    for nn in (2, 4):
+        with dd.GroupJacobi("XL", [0] * 8) as g:
+            gosa = g.jacobi(nn)
+            p = g.gather("p")
+        want_p, want_g = xl_oracle[nn]
+        assert np.array_equal(p, want_p), (overlap, nn)
+        assert abs(gosa - want_g) <= 1e-11 * want_g, (overlap, nn)
+        del p

@@ -21,6 +21,7 @@
 //    and one ncclAllReduce of gosa, on the context's stream.  libnccl.so.2 is
 //    dlopen'ed on first use (the library has no link-time NCCL dependency; an
 //    NCCL already loaded by torch is reused).
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -122,6 +123,62 @@ static int dd_reserve() {
   return e ? atoi(e) : 8;
 }
 
+// cuStreamWaitValue32 (driver API, via the runtime's entry-point query): the exchange
+// stream waits until a device counter reaches a value -- the boundary units of a
+// signalled slab pass bump it from inside the running kernel.  nullptr if unavailable.
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value32() {
+  static WaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<WaitValue32Fn>(p);
+    cudaGetLastError();
+    return (WaitValue32Fn) nullptr;
+  }();
+  return fn;
+}
+
+// HIMENO_DD_SIGNAL=0: overlapped passes as two launches (boundary, then interior) with an
+// event between them instead of one signalled launch.  Read per call (tests switch it).
+static bool dd_signal() {
+  const char* e = getenv("HIMENO_DD_SIGNAL");
+  return !(e && atoi(e) == 0) && wait_value32() != nullptr;
+}
+
+// Boundary counter of one slab context (signalled passes): device word + the value the
+// next wait targets.  Reset to 0 between passes when the target nears 2^31 (safe then:
+// the compute stream has already waited for the previous exchange).
+struct Signal {
+  unsigned* dev = nullptr;
+  unsigned target = 0;
+};
+
+// One signalled pass: one launch, boundary units first; returns kernels launched (1), 0
+// if not applicable, -1 on error.  On success sig->target is the count to wait for.
+static int slab_pass_signaled(hp_ctx* c, const float* in, float* out, const LaunchArgs& a,
+                              int reserve, Signal* sig) {
+  if (!sig || !sig->dev || !dd_signal()) return 0;
+  if (sig->target > (1u << 30)) {
+    if (cudaMemsetAsync(sig->dev, 0, sizeof(unsigned), c->stream) != cudaSuccess) return -1;
+    sig->target = 0;
+  }
+  int nb = 0;
+  const int r = launch_stencil_tb2_signaled(c->dev, c->dev.tma, in, out, a, c->sink(), c->stream,
+                                            sm_count_of(c), reserve, sig->dev, &nb);
+  if (r > 0) sig->target += (unsigned)nb;
+  return r;
+}
+
+// Make `xs` wait for a signalled pass's boundary units (value >= target).
+static cudaError_t gate_on_signal(cudaStream_t xs, const Signal& sig) {
+  const CUresult r = wait_value32()(reinterpret_cast<CUstream>(xs),
+                                    reinterpret_cast<CUdeviceptr>(sig.dev), sig.target,
+                                    CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
 // One pass on a slab, split into boundary + interior when overlapping; `bdone` is
 // recorded on the compute stream after the planes the neighbours need are written.
 static int slab_pass_overlapped(hp_ctx* c, const float* in, float* out, int step,
@@ -164,14 +221,23 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     if (rc == HP_OK) rc = cuda_fail(e, what);
   };
   const bool overlap = dd_overlap() != 0 && n > 1;
+  // signalled passes (one launch, the exchange waits on a counter the boundary units bump)
+  // when every slab is on one device (the counters are then local to every stream)
+  bool one_device = true;
+  for (int r = 1; r < n; ++r) one_device = one_device && ctxs[r]->device == ctxs[0]->device;
+  std::vector<Signal> sig(n);
+  const bool signaled = overlap && one_device && dd_signal();
   for (int r = 0; r < n && rc == HP_OK; ++r) {
     cudaSetDevice(ctxs[r]->device);
     cudaError_t e = cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hin[r], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&comm[r], cudaStreamNonBlocking);
+    if (e == cudaSuccess && signaled) e = cudaMalloc(&sig[r].dev, sizeof(unsigned));
+    if (e == cudaSuccess && signaled) e = cudaMemset(sig[r].dev, 0, sizeof(unsigned));
     if (e != cudaSuccess) fail(e, "event / stream create");
     else if (time_loop_begin(ctxs[r], ctx_args(ctxs[r], 1)) < 0) fail(cudaGetLastError(), "begin");
   }
+  std::vector<char> gated(n, 0);   // this pass's exchange gates on the counter, not `done`
   int pass = 0;
   for (int it = 0; it < nn && rc == HP_OK; ++pass) {
     const int step = pass_step(it, nn);
@@ -183,8 +249,18 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
         cudaError_t e = cudaStreamWaitEvent(c->stream, hin[r], 0);
         if (e != cudaSuccess) fail(e, "wait halo");
       }
-      const int k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step,
-                                         ctx_args(c, 1), overlap, 0, done[r]);
+      int k = 0;
+      gated[r] = 0;
+      if (signaled && step == 2) {
+        k = slab_pass_signaled(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), ctx_args(c, 1),
+                               0, &sig[r]);
+        gated[r] = k > 0;
+      }
+      if (k == 0)
+        k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step,
+                                 ctx_args(c, 1), overlap, 0, done[r]);
+      else if (k > 0 && cudaEventRecord(done[r], c->stream) != cudaSuccess)   // end of pass
+        k = -1;
       if (k < 0) fail(cudaGetLastError(), "stencil pass");
       c->launches += k > 0 ? k : 0;
     }
@@ -194,7 +270,10 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
       hp_ctx* c = ctxs[r];
       cudaSetDevice(c->device);
       float* out = pass_buffer(c, pass + 1);
-      cudaError_t e = cudaStreamWaitEvent(comm[r], done[r], 0);   // WAR: this pass's reads
+      // WAR: the receiver's previous pass no longer reads these halo planes once its
+      // current pass runs (its boundary units counted / `done` recorded)
+      cudaError_t e = gated[r] ? gate_on_signal(comm[r], sig[r])
+                               : cudaStreamWaitEvent(comm[r], done[r], 0);
       for (int side = -1; side <= 1 && rc == HP_OK; side += 2) {
         const int q = r + side;
         if (q < 0 || q >= n) continue;
@@ -203,7 +282,8 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
         // lower halo <- neighbour's last two interior planes; upper <- its first two
         const int dst_plane = side < 0 ? c->li_lo - kHalo : c->li_hi;
         const int src_plane = side < 0 ? nb->li_hi - kHalo : nb->li_lo;
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(comm[r], done[q], 0);
+        if (e == cudaSuccess)
+          e = gated[q] ? gate_on_signal(comm[r], sig[q]) : cudaStreamWaitEvent(comm[r], done[q], 0);
         if (e == cudaSuccess)
           e = cudaMemcpyPeerAsync(plane_ptr(c, out, dst_plane), c->device,
                                   plane_ptr(nb, nb_out, src_plane), nb->device,
@@ -245,6 +325,7 @@ extern "C" int hp_group_jacobi(hp_ctx** ctxs, int n, int nn, double* gosa_out) {
     }
     if (done[r]) cudaEventDestroy(done[r]);
     if (hin[r]) cudaEventDestroy(hin[r]);
+    if (sig[r].dev) cudaFree(sig[r].dev);
   }
   if (rc == HP_OK && gosa_out) *gosa_out = total;
   return rc;
@@ -305,6 +386,7 @@ struct DD {
   cudaStream_t xs = nullptr;      // halo exchange stream (overlapped with the interior)
   cudaEvent_t bdone = nullptr;    // boundary planes of the current pass written
   cudaEvent_t hin = nullptr;      // halos of the current pass received
+  Signal sig;                     // signalled passes: boundary-unit counter
 };
 
 int nccl_fail(ncclResult_t r, const char* what) {
@@ -323,6 +405,7 @@ void hp::dd_destroy(hp_ctx* c) {
   }
   if (d && d->bdone) cudaEventDestroy(d->bdone);
   if (d && d->hin) cudaEventDestroy(d->hin);
+  if (d && d->sig.dev) cudaFree(d->sig.dev);
   delete d;
   c->dd = nullptr;
 }
@@ -374,7 +457,9 @@ extern "C" int hp_dd_init(hp_ctx* c, int nranks, int rank, const unsigned char* 
   cudaSetDevice(c->device);
   if (cudaStreamCreateWithFlags(&d->xs, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&d->bdone, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&d->hin, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&d->hin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&d->sig.dev, sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(d->sig.dev, 0, sizeof(unsigned)) != cudaSuccess) {
     c->dd = d;
     dd_destroy(c);
     return cuda_fail(cudaGetLastError(), "hp_dd_init streams");
@@ -405,14 +490,22 @@ extern "C" int hp_dd_jacobi(hp_ctx* c, int nn) {
       const cudaError_t e = cudaStreamWaitEvent(c->stream, d->hin, 0);
       if (e != cudaSuccess) return cuda_fail(e, "wait halo");
     }
-    const int k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, a,
-                                       overlap, reserve, d->bdone);
+    int k = 0;
+    bool gated = false;
+    if (overlap && step == 2) {   // one launch, the exchange gated on the boundary counter
+      k = slab_pass_signaled(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), a, reserve,
+                             &d->sig);
+      gated = k > 0;
+    }
+    if (k == 0)
+      k = slab_pass_overlapped(c, pass_buffer(c, pass), pass_buffer(c, pass + 1), step, a,
+                               overlap, reserve, d->bdone);
     if (k < 0) return cuda_fail(cudaGetLastError(), "stencil pass");
     c->launches += k;
     it += step;
     if (!l) continue;
     // halo exchange on the exchange stream once the boundary planes are written
-    cudaError_t e = cudaStreamWaitEvent(d->xs, d->bdone, 0);
+    cudaError_t e = gated ? gate_on_signal(d->xs, d->sig) : cudaStreamWaitEvent(d->xs, d->bdone, 0);
     if (e != cudaSuccess) return cuda_fail(e, "wait boundary");
     float* out = pass_buffer(c, pass + 1);
     ncclResult_t r = l->GroupStart();

@@ -117,6 +117,11 @@ int launch_stencil_tb2(const DevFields& F, const void* h, const float* p_in, flo
 int launch_stencil_tb2_part(const DevFields& F, const void* h, const float* p_in, float* p_out,
                             const LaunchArgs& a, const GosaSink& g, cudaStream_t s, int sms,
                             int part, int reserve);
+// one two-step pass of a slab as one launch, boundary units first, each counted in
+// *sig as it finishes (*nb_out = boundary units); 0 = slab too thin
+int launch_stencil_tb2_signaled(const DevFields& F, const void* h, const float* p_in,
+                                float* p_out, const LaunchArgs& a, const GosaSink& g,
+                                cudaStream_t s, int sms, int reserve, unsigned* sig, int* nb_out);
 // `passes` >= 2 two-step passes in ONE launch (units of pass t+1 start as soon as
 // their neighbourhood in pass t is done); result in p_out if passes is odd, else
 // p_in; 0 = not applicable (caller launches pass by pass)

@@ -111,16 +111,24 @@ struct Unit {           // one contiguous run of planes of one tile
 // Two-range mode (r2_hi > r2_lo, two-step kernel only): exactly two plane ranges per
 // tile, [0, ni) and [r2_lo, r2_hi) relative to i_lo -- a slab's two boundary plane
 // pairs in one launch (decomp.cpp, halo exchange overlapped with the interior).
+// Boundary-prefix mode (sw > 0, two-step kernel, decomp.cpp): the first 2 * tiles units
+// are the slab's boundary plane blocks [0, sw) and [ni - sw, ni) of every tile -- what the
+// neighbouring slabs need -- and the usual whole-column / chunk units follow over the
+// interior [sw, ni - sw).  One launch; the boundary units signal as they finish.
 struct Units {
   int ni, ktiles, tiles, len, full;
   uint32_t count;
   int r2_lo, r2_hi;
+  int sw;        // boundary-prefix width (planes), 0 = off
+  uint32_t nb;   // boundary units (2 * tiles when sw > 0)
   __device__ Units(int ni_, int ktiles_, int tiles_, int len_, int full_, int r2_lo_ = 0,
-                   int r2_hi_ = 0)
+                   int r2_hi_ = 0, int sw_ = 0)
       : ni(ni_), ktiles(ktiles_), tiles(tiles_), len(len_), full(r2_hi_ > r2_lo_ ? 0 : full_),
-        count(r2_hi_ > r2_lo_ ? (uint32_t)(2 * tiles_)
-                              : (uint32_t)(full_ + (tiles_ - full_) * ((ni_ + len_ - 1) / len_))),
-        r2_lo(r2_lo_), r2_hi(r2_hi_) {}
+        count(r2_hi_ > r2_lo_
+                  ? (uint32_t)(2 * tiles_)
+                  : (uint32_t)((sw_ > 0 ? 2 * tiles_ : 0) + full_ +
+                               (tiles_ - full_) * ((ni_ - 2 * sw_ + len_ - 1) / len_))),
+        r2_lo(r2_lo_), r2_hi(r2_hi_), sw(sw_), nb(sw_ > 0 ? (uint32_t)(2 * tiles_) : 0u) {}
   __device__ void decode(uint32_t u, Unit& s) const {
     int t, c;
     if (r2_hi > r2_lo) {
@@ -128,16 +136,21 @@ struct Units {
       c = (int)(u / (uint32_t)tiles);
       s.ia = c ? r2_lo : 0;
       s.ib = c ? r2_hi : ni;
-    } else if (u < (uint32_t)full) {
-      t = (int)u;
-      s.ia = 0;
-      s.ib = ni;
+    } else if (u < nb) {
+      t = (int)(u % (uint32_t)tiles);
+      c = (int)(u / (uint32_t)tiles);
+      s.ia = c ? ni - sw : 0;
+      s.ib = c ? ni : sw;
+    } else if (u - nb < (uint32_t)full) {
+      t = (int)(u - nb);
+      s.ia = sw;
+      s.ib = ni - sw;
     } else {
-      const uint32_t v = u - (uint32_t)full, rest = (uint32_t)(tiles - full);
+      const uint32_t v = u - nb - (uint32_t)full, rest = (uint32_t)(tiles - full);
       t = full + (int)(v % rest);
       c = (int)(v / rest);
-      s.ia = c * len;
-      s.ib = min(ni, s.ia + len);
+      s.ia = sw + c * len;
+      s.ib = min(ni - sw, s.ia + len);
     }
     s.kt = t % ktiles;
     s.jt = t / ktiles;
@@ -368,6 +381,8 @@ struct Flow {
   float* out[2];       // pass t writes out[t & 1] (and reads the other buffer)
   unsigned* done;      // [upp]: unit v of pass t complete <=> done[v] >= tag0 + t + 1
   unsigned tag0;       // launch epoch * 4096
+  int split;           // boundary-prefix width (planes) of a signalled slab pass, 0 = off
+  unsigned* sig;       // incremented once per finished boundary unit (split > 0)
 };
 
 // p0 tile row (PW0 floats): sub-lane quad at column 4 + 4*hl (k0-4+4*hl), edges at
@@ -662,6 +677,19 @@ __device__ void unit_finish(const GosaSink& g, uint32_t u, uint32_t upp, const F
                  : "memory");
   }
 }
+// A boundary unit of a signalled slab pass is written: count it.  The halo exchange's
+// stream waits for the count (cuStreamWaitValue32) and then copies / sends the planes, so
+// the stores must be visible beyond the SMs (copy engines, NCCL): system-scope fence.
+// Called by every step-2 thread after unit_finish's named barrier.
+__device__ __forceinline__ void boundary_signal(const Flow& fl, bool boundary, int wrel, int nw,
+                                                int bar) {
+  if (!fl.sig || !boundary) return;
+  named_bar_sync(bar, nw * 32);   // every step-2 warp's stores of the unit are issued
+  if (wrel == 0 && (threadIdx.x & 31) == 0) {
+    __threadfence_system();
+    atomicAdd_system(fl.sig, 1u);
+  }
+}
 
 // CPOL_ = 1: the coefficient TMA loads carry an L2 evict_first policy.  The flow launch
 // (several passes in flight, small grids) runs 2.7 % faster with it on M; on L, whose
@@ -697,7 +725,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
   const int jtiles = (j_hi - j_lo + TJ2 - 1) / TJ2;
-  const Units units(ni, ktiles, ktiles * jtiles, chunk, full, i_lo2 - i_lo, i_hi2 - i_lo);
+  const Units units(ni, ktiles, ktiles * jtiles, chunk, full, i_lo2 - i_lo, i_hi2 - i_lo, fl.split);
   const uint32_t nunits = units.count * (uint32_t)fl.passes;   // queue: pass-major
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
@@ -971,6 +999,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         zm = nm; z0 = n0; zp = np;
       }
       unit_finish(g, u, units.count, fl, acc, unit_part, warp - NW1, NW2, 1);
+      boundary_signal(fl, (u % units.count) < units.nb, warp - NW1, NW2, 1);
       acc = 0.0;
     }
   } else {
@@ -1039,6 +1068,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
       // stage of plane ib carries no output plane either
       if (lane == 0) mbar_arrive(&cempty[(sc - 1) % SC]);
       unit_finish(g, u, units.count, fl, acc, unit_part, warp - NW1, NW2, 1);
+      boundary_signal(fl, (u % units.count) < units.nb, warp - NW1, NW2, 1);
       acc = 0.0;
     }
   }
@@ -1376,6 +1406,9 @@ static Tb2Choice tb2_choose(int ni, int nj, int k_hi, int sms) {
 struct Range2 {
   int lo = 0, hi = 0;   // second output plane range (two-range launch), empty if hi <= lo
   int grid_cap = 0;     // > 0: at most this many CTAs (SMs left to a concurrent kernel)
+  int split = 0;        // > 0: boundary-prefix units of this width (signalled slab pass)
+  unsigned* sig = nullptr;
+  int* nb_out = nullptr;   // receives the number of boundary units (signal target step)
 };
 
 template <int LW, int NW1, int SC, bool ST = false, int CPOL = 0>
@@ -1390,8 +1423,15 @@ static int launch_tb2(const Tb2Maps& maps, const DevFields& F, Flow fl, int i_lo
   const long long tiles = (long long)ktiles * jtiles;
   if (full < 0 || full > tiles) full = 0;
   const bool two = r2.hi > r2.lo;
+  const int sw = two ? 0 : r2.split;
   const long long units =
-      two ? 2 * tiles : full + (tiles - full) * ((i_hi - i_lo + chunk - 1) / chunk);
+      two ? 2 * tiles
+          : (sw > 0 ? 2 * tiles : 0) + full + (tiles - full) * ((i_hi - i_lo - 2 * sw + chunk - 1) / chunk);
+  if (sw > 0) {
+    fl.split = sw;
+    fl.sig = r2.sig;
+    if (r2.nb_out) *r2.nb_out = (int)(2 * tiles);
+  }
   long long grid = sms;
   if (r2.grid_cap > 0 && grid > r2.grid_cap) grid = r2.grid_cap;
   if (grid > units * fl.passes) grid = units * fl.passes;
@@ -1650,6 +1690,26 @@ int launch_stencil_tb2_part(const DevFields& F, const void* h, const float* p_in
     r2.grid_cap = reserve > 0 ? std::max(1, sms - reserve) : sms;
   }
   return launch_two_step(F, h, p_in, p_out, 1, b, g, s, sms, r2);
+}
+
+// One two-step pass of a slab as ONE launch whose first units are the boundary plane
+// pairs (decomp.cpp): each finished boundary unit increments *sig, so the halo exchange
+// can start (cuStreamWaitValue32 on the exchange stream) while the interior units run;
+// *nb_out = boundary units per pass (the signal target step).  At most sms - reserve
+// CTAs.  Returns 1, 0 (slab too thin: caller splits or runs the whole pass), or -1.
+int launch_stencil_tb2_signaled(const DevFields& F, const void* h, const float* p_in,
+                                float* p_out, const LaunchArgs& a, const GosaSink& g,
+                                cudaStream_t s, int sms, int reserve, unsigned* sig, int* nb_out) {
+  if (a.li_hi - a.li_lo < 6 || !sig || !nb_out) return 0;
+  Range2 r2;
+  r2.split = 2;
+  r2.sig = sig;
+  r2.nb_out = nb_out;
+  r2.grid_cap = reserve > 0 ? std::max(1, sms - reserve) : sms;
+  *nb_out = 0;
+  const int r = launch_two_step(F, h, p_in, p_out, 1, a, g, s, sms, r2);
+  if (r > 0 && *nb_out <= 0) return -1;
+  return r;
 }
 
 // Flow launches pay where the per-pass drain matters: when one pass's tiles fit in

@@ -12,11 +12,11 @@ from paper_2002_12115_b200 import dd  # noqa: E402
 for ranks in (8, 4):
     with dd.GroupJacobi("L", [0] * ranks) as g:
         for rep in range(2):
-            for conf in (("1", "0"), ("0", "0"), ("0", "1")):
-                os.environ["HIMENO_DD_OVERLAP"], os.environ["HIMENO_TX"] = conf
+            for conf in (("1", "0", "1"), ("1", "0", "0"), ("0", "0", "1"), ("0", "1", "1")):
+                os.environ["HIMENO_DD_OVERLAP"], os.environ["HIMENO_TX"], os.environ["HIMENO_DD_SIGNAL"] = conf
                 g.jacobi(8)
                 t0 = time.perf_counter()
                 g.jacobi(40)
                 el = time.perf_counter() - t0
-                print(f"L/{ranks} overlap={conf[0]} tx={conf[1]}: {el * 1e3 / 20:.3f} ms per two-step pass "
+                print(f"L/{ranks} overlap={conf[0]} tx={conf[1]} signal={conf[2]}: {el * 1e3 / 20:.3f} ms per two-step pass "
                       f"(all {ranks} slabs on one GPU)", flush=True)

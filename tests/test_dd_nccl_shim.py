@@ -75,10 +75,13 @@ def shim(tmp_path_factory):
 @pytest.mark.gpu
 @pytest.mark.parametrize("ranks,name,nn,tb,overlap", [
     (2, "XS", 4, 1, 1), (3, "XS", 5, 1, 1), (2, "XS", 3, 0, 0),
-    (4, "M", 6, 1, 1), (2, "M", 4, 1, 0),
+    (4, "M", 6, 1, 1), (2, "M", 4, 1, 0), (3, "M", 6, 1, 2),
 ])
 def test_nccl_transport_multi_rank_one_gpu(gpu, shim, ranks, name, nn, tb, overlap):
-    env = dict(os.environ, HIMENO_NCCL_LIB=str(shim), HIMENO_DD_OVERLAP=str(overlap))
+    # overlap 1: one signalled launch per pass (cuStreamWaitValue32 gates the exchange);
+    # 2: two launches (boundary, interior) and an event; 0: exchange after the pass
+    env = dict(os.environ, HIMENO_NCCL_LIB=str(shim), HIMENO_DD_OVERLAP=str(min(overlap, 1)),
+               HIMENO_DD_SIGNAL="0" if overlap == 2 else "1")
     script = SCRIPT.format(root=str(ROOT), ranks=ranks, name=name, nn=nn, tb=tb)
     proc = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True,
                           text=True, timeout=600)

@@ -509,7 +509,7 @@ def l_oracle_n4():
     return {3: (p3, g3), 4: (f["p"].copy(), g4)}
 
 
-@pytest.mark.parametrize("overlap", [0, 1])
+@pytest.mark.parametrize("overlap", [0, 1, 2])
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("ranks", [2, 4, 8])
 def test_l_grid_slabs_bit_exact(gpu, monkeypatch, l_oracle_n4, ranks, tb, overlap):
@@ -518,7 +518,10 @@ def test_l_grid_slabs_bit_exact(gpu, monkeypatch, l_oracle_n4, ranks, tb, overla
     a comm stream -- and gosa sum after the passes) with virtual ranks on one GPU,
     against the full grid."""
     from paper_2002_12115_b200 import dd
-    monkeypatch.setenv("HIMENO_DD_OVERLAP", str(overlap))
+    # 0: exchange after each whole pass; 1: overlapped, one launch whose boundary units
+    # signal the exchange stream; 2: overlapped as two launches (boundary, interior)
+    monkeypatch.setenv("HIMENO_DD_OVERLAP", str(min(overlap, 1)))
+    monkeypatch.setenv("HIMENO_DD_SIGNAL", "0" if overlap == 2 else "1")
     lib = N.load()
     old = lib.hp_set_temporal_blocking(tb)
     try:

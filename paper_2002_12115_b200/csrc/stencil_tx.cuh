@@ -34,7 +34,7 @@
 //
 // Co-residency: a CTA waits on its neighbours, so all CTAs of a launch must be
 // resident together: grid <= SMs, one CTA per SM (217 KB of shared memory), and
-// exchange launches on one device are serialised across contexts (tx_order).
+// exchange launches on one device are chained across streams (launch_tx in stencil_tma.cu).
 // A neighbour wait that exceeds 2 s (never expected) records an error instead of
 // hanging: gosa becomes NaN and hp_tx_status reports it.
 //

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("measurements")
     ap.add_argument("--out")
     ap.add_argument("--latency", type=float, default=1e-5)
+    ap.add_argument("--bandwidth", type=float,
+                    help="bytes/s of a transfer event when the table has no transfer stats "
+                         "(e.g. 2.075e10, measured in profiles/r01_evalall_M.jsonl)")
     args = ap.parse_args()
     prog = himeno.program()
     loops, refs, elig = prog.model.loops, prog.model.refs, list(prog.eligible)
@@ -31,7 +34,7 @@ def main():
     rows = [r for r in rows if not r.get("summary") and r.get("time_s")]
     moved = sum((r.get("h2d_bytes") or 0) + (r.get("d2h_bytes") or 0) for r in rows)
     blocked = sum(r.get("xfer_s") or 0 for r in rows)
-    bw = moved / blocked if blocked > 0 else 2.5e10
+    bw = moved / blocked if blocked > 0 else (args.bandwidth or 2.5e10)
     samples = [(tuple(int(c) for c in r["genome"]), float(r["time_s"])) for r in rows]
     meas = [t for _, t in samples]
     best_meas = min(samples, key=lambda s: s[1])

@@ -1109,9 +1109,18 @@ struct TmaState {
   unsigned* done = nullptr;
   int done_cap = 0;
   unsigned flow_epoch = 0;
+  // maps whose k / j extents stop at K-1 / J-1 (HIMENO_TMA_TRIM bits: 1 two-step, 2
+  // single-step, 4 exchange kernel); launches need kmax <= K-1 and jmax <= J-1
+  int trim = 0;
 };
 
 }  // namespace
+
+// integer environment knob, -1 when unset
+static int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : -1;
+}
 
 // Build the tensor maps of one context (fields + rotation scratch); nullptr if
 // the driver cannot encode them (the caller then uses k_stencil_3d).
@@ -1132,20 +1141,30 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   int dk = F.K;
   if (const char* e = getenv("HIMENO_TMA_DIMK")) dk = atoi(e) ? F.K : F.P;
   bool ok = true;
+  // The program never touches column K-1 or row J-1 (kmax = K-1, jmax = J-1: its
+  // loops and step-1 halos end at K-2 / J-2), but a box reaching the row end would
+  // still fetch the 128-byte line that holds column K-1 -- on L one extra line per
+  // 16 per row, 0.12 GB of a pass's 1.90 GB DRAM reads (1.11x -> 1.04x algorithmic;
+  // L pass -0.6 %, M -0.9 %, XL -5 %; profiles/r02_tb2_experiments_late.md).  Maps end
+  // there unless HIMENO_TMA_TRIM clears the bit.
+  const int trim_env = env_int("HIMENO_TMA_TRIM");
+  t->trim = F.K >= 4 && F.J >= 4 ? (trim_env < 0 ? 7 : trim_env & 7) : 0;
+  const int dk1 = (t->trim & 2) ? F.K - 1 : dk, dj1 = (t->trim & 2) ? F.J - 1 : 0;
   for (int m = 0; m < NCOEF; ++m) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
-    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ, pc[0], dk);
+    ok = ok && encode(&t->base.coef[m], F, F.f[fields[m]], TK, TJ, pc[0], dk1, dj1);
   }
-  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1], dk);
-  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1], dk);
+  ok = ok && encode(&t->base.pin, F, F.f[HP_F_P], PW, PH, pc[1], dk1, dj1);
+  ok = ok && encode(&t->scratch_map, F, scratch, PW, PH, pc[1], dk1, dj1);
+  const int dk2 = (t->trim & 1) ? F.K - 1 : dk, dj2 = (t->trim & 1) ? F.J - 1 : 0;
   auto encode_tb2 = [&](Tb2Maps& maps, CUtensorMap& scr, int qk, int r1) {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
     for (int m = 0; m < NCOEF; ++m)
-      ok = ok && encode(&maps.coef[m], F, F.f[fields[m]], qk, r1, pc[2], dk);
-    ok = ok && encode(&maps.pin, F, F.f[HP_F_P], qk + 8, r1 + 2, pc[3], dk);
-    ok = ok && encode(&scr, F, scratch, qk + 8, r1 + 2, pc[3], dk);
+      ok = ok && encode(&maps.coef[m], F, F.f[fields[m]], qk, r1, pc[2], dk2, dj2);
+    ok = ok && encode(&maps.pin, F, F.f[HP_F_P], qk + 8, r1 + 2, pc[3], dk2, dj2);
+    ok = ok && encode(&scr, F, scratch, qk + 8, r1 + 2, pc[3], dk2, dj2);
   };
   encode_tb2(t->tb2[0], t->tb2_scratch[0], Tb2<32, 8, 4>::QK, Tb2<32, 8, 4>::R1);
   encode_tb2(t->tb2[1], t->tb2_scratch[1], Tb2<16, 8, 4>::QK, Tb2<16, 8, 4>::R1);
@@ -1154,10 +1173,11 @@ void* create_stencil_tma(const DevFields& F, const float* scratch) {
   {
     static const int fields[NCOEF] = {HP_F_A0, HP_F_A1, HP_F_A2, HP_F_A3, HP_F_B0, HP_F_B1,
                                       HP_F_B2, HP_F_C0, HP_F_C1, HP_F_C2, HP_F_WRK1, HP_F_BND};
+    const int dk3 = (t->trim & 4) ? F.K - 1 : dk, dj3 = (t->trim & 4) ? F.J - 1 : 0;
     for (int m = 0; m < NCOEF; ++m)
-      ok = ok && encode(&t->tx.coef[m], F, F.f[fields[m]], XK, kTxTJ, pc[2], dk);
-    ok = ok && encode(&t->tx.pin, F, F.f[HP_F_P], XW, kTxTJ + 2, pc[3], dk);
-    ok = ok && encode(&t->tx_scratch, F, scratch, XW, kTxTJ + 2, pc[3], dk);
+      ok = ok && encode(&t->tx.coef[m], F, F.f[fields[m]], XK, kTxTJ, pc[2], dk3, dj3);
+    ok = ok && encode(&t->tx.pin, F, F.f[HP_F_P], XW, kTxTJ + 2, pc[3], dk3, dj3);
+    ok = ok && encode(&t->tx_scratch, F, scratch, XW, kTxTJ + 2, pc[3], dk3, dj3);
   }
   t->p = F.f[HP_F_P];
   t->scratch = scratch;
@@ -1266,6 +1286,7 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
                        int sms) {
   const TmaState* t = static_cast<const TmaState*>(h);
   if (!t || (p_in != t->p && p_in != t->scratch)) return 0;
+  if ((t->trim & 2) && (a.kmax > F.K - 1 || a.jmax > F.J - 1)) return 0;
   const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
             k_hi = a.kmax - 1;
   if (i_hi <= i_lo || j_hi <= j_lo || k_hi <= k_lo) return 0;
@@ -1305,10 +1326,6 @@ int launch_stencil_tma(const DevFields& F, const void* h, const float* p_in, flo
 //   3 = (16, 5, 6):  64 x 10 step-1 tile, 56 x 8 outputs, 30 KB stages
 // The shape and the planes per work unit are chosen per pass geometry by a
 // scheduling model (tb2_choose below).
-static int env_int(const char* name) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : -1;
-}
 
 // First output column of k-tile 0.  -4 puts every tile's coefficient boxes (origin
 // k0-4) on a 32-byte sector boundary: 8 sectors per 64-column row instead of 9
@@ -1503,6 +1520,7 @@ static int launch_tx(TmaState* t, const DevFields& F, const float* p_in, float* 
   const int mode = tx_mode();
   // a pinned two-step shape (sweeps, tests) asks for k_stencil_tb2
   if (mode == 0 || !t->xr || env_int("HIMENO_TB2_SHAPE") >= 0) return 0;
+  if ((t->trim & 4) && (a.kmax > F.K - 1 || a.jmax > F.J - 1)) return 0;
   const int ktiles = (k_hi + XK - 1) / XK;
   const int jtiles = (j_hi - j_lo + TJ - 1) / TJ;
   const int tiles = ktiles * jtiles;
@@ -1590,6 +1608,7 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
                            int sms, const Range2& r2 = Range2{}) {
   TmaState* t = const_cast<TmaState*>(static_cast<const TmaState*>(h));
   if (!t || (p_in != t->p && p_in != t->scratch) || passes < 1) return 0;
+  if ((t->trim & 1) && (a.kmax > F.K - 1 || a.jmax > F.J - 1)) return 0;
   const int i_lo = a.li_lo, i_hi = a.li_hi, j_lo = 1, j_hi = a.jmax - 1, k_lo = 1,
             k_hi = a.kmax - 1;
   // step 1 reads p0 two planes beyond the planes it updates: the full grid (plane

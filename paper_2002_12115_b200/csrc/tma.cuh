@@ -179,11 +179,11 @@ inline CUtensorMapL2promotion promo(int code) {
 }
 
 inline bool encode(CUtensorMap* m, const DevFields& F, const float* base, uint32_t box_k,
-                   uint32_t box_j, int promo_code = 2, int dim_k = 0) {
+                   uint32_t box_j, int promo_code = 2, int dim_k = 0, int dim_j = 0) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)(dim_k > 0 ? dim_k : F.P), (cuuint64_t)F.J,
-                              (cuuint64_t)F.I};
+  const cuuint64_t dims[3] = {(cuuint64_t)(dim_k > 0 ? dim_k : F.P),
+                              (cuuint64_t)(dim_j > 0 ? dim_j : F.J), (cuuint64_t)F.I};
   const cuuint64_t strides[2] = {(cuuint64_t)F.P * 4, (cuuint64_t)F.plane() * 4};
   const cuuint32_t box[3] = {box_k, box_j, 1};
   const cuuint32_t estr[3] = {1, 1, 1};

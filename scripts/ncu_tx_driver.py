@@ -1,5 +1,5 @@
 """Small driver for ncu: L grid, one jacobi(4) (two two-step passes) on the default
-two-step kernel (HIMENO_TX decides which)."""
+two-step kernel (HIMENO_TX decides which), or k_stencil_tma<3> with HIMENO_SINGLE_STEP=1."""
 import os
 import sys
 
@@ -8,6 +8,8 @@ from paper_2002_12115_b200 import native as N  # noqa: E402
 from paper_2002_12115_b200.apps import himeno  # noqa: E402
 
 sz = himeno.size(sys.argv[1] if len(sys.argv) > 1 else "L")
+if os.environ.get("HIMENO_SINGLE_STEP"):   # the one-iteration kernel k_stencil_tma<3>
+    N.load().hp_set_temporal_blocking(0)
 with N.Context(0, sz.I, sz.J, sz.K) as ctx:
     ctx.init_device()
     ctx.jacobi_device(4, 1)

@@ -725,3 +725,34 @@ def test_xl_grid_8_slabs_bit_exact(gpu, monkeypatch, xl_oracle, overlap):
         assert np.array_equal(p, want_p), (overlap, nn)
         assert abs(gosa - want_g) <= 1e-11 * want_g, (overlap, nn)
         del p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("trim", ["0", "7"])
+@pytest.mark.parametrize("kernel", ["tb2", "single", "tx"])
+@pytest.mark.parametrize("dims", [(33, 33, 65), (37, 21, 70), (45, 47, 121), (20, 20, 58)])
+def test_trimmed_tma_extents_bit_exact(gpu, monkeypatch, dims, kernel, trim):
+    """Tensor maps ending at column K-1 / row J-1 (the default) or at K / J give the
+    oracle's field bit for bit in every stencil kernel (ragged and tile-multiple grids)."""
+    sz = himeno.custom_size(*dims)
+    nn = 4
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    monkeypatch.setenv("HIMENO_TMA_TRIM", trim)
+    if kernel == "tx":
+        monkeypatch.setenv("HIMENO_TX", "2")
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(0 if kernel == "single" else 1)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            used = N.last_two_step_kernel()
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
+    if kernel == "tx":
+        assert used == "k_stencil_tx"
+    elif kernel == "tb2":
+        assert used.startswith("k_stencil_tb2")
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]

@@ -538,7 +538,7 @@ def run_ours(args, world, rank, local):
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": (f"{two_step_kernel} (temporal blocking: 2 iterations per pass, 56 B/pt "
                            "per pass; warp-specialised TMA pipeline, step-2 coefficients "
-                           "stashed in tensor memory)"
+                           "handed over in tensor memory by the step-1 warps)"
                            if variant == 1 and kt.stencil_iters > 1.5 else "k_stencil_tma<3>"),
                 "bytes_per_point": BYTES_STENCIL, "points_per_launch": points,
                 "passes_per_launch": launch_bytes(points, kt.stencil_iters) / (BYTES_STENCIL * points),

@@ -719,8 +719,18 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   UnitRing* ring = reinterpret_cast<UnitRing*>(qempty + SQ);
   __shared__ double unit_part[NW2];
   __shared__ uint32_t tmem_base_s;   // ST: tensor-memory stash of the step-2 coefficients
-  constexpr uint32_t kStashCols = 256;
+  // CPOL_ & 4 (XS, "cross-warp stash"): the step-1 warps, which load every coefficient
+  // quad from shared memory anyway, write the quads of rows 1..14 into tensor memory and
+  // the step-2 warps read them from there -- no second shared-memory read of the
+  // coefficients.  Step-1 warp w < 7 takes rows 2w+1, 2w+2 (warp 7 the halo rows 0 and
+  // 15), so step-2 warp w2 needs exactly step-1 warp w2's quads, in the same TMEM lanes
+  // (warps 8+w2 and w2 share the lane quarter w2 % 4).  Five stash slots per plane ring.
+  constexpr bool XS = (CPOL_ & 4) != 0;
+  constexpr uint32_t kStashCols = XS ? 512 : 256;
+  constexpr int kXSlots = 5;
   static_assert(!ST_ || (NW1 % 4 == 0 && NW2 <= 8), "stash: (warp%4, block) per step-2 warp");
+  static_assert(!XS || (ST_ && NW1 == 8 && RPW == 2 && NW2 == 7 && SQ == 4),
+                "cross-warp stash: shape (16, 8, 4) with the p1 ring of 4 (WAR via qempty)");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hl = lane % LW, half = lane / LW;   // lane within the row, row within the warp
   const int ni = i_hi - i_lo;
@@ -729,7 +739,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   const uint32_t nunits = units.count * (uint32_t)fl.passes;   // queue: pass-major
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP; ++s) { mbar_init(&pfull[s], 1); mbar_init(&pempty[s], NW1); }
-    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], NW1 + NW2); }
+    for (int s = 0; s < SC; ++s) { mbar_init(&cfull[s], 1); mbar_init(&cempty[s], XS ? NW1 : NW1 + NW2); }
     // p1 ring: every thread arrives (no reliance on __syncwarp ordering for the
     // shared-memory rows written / read by other warps)
     for (int s = 0; s < SQ; ++s) { mbar_init(&qfull[s], NW1 * 32); mbar_init(&qempty[s], NW2 * 32); }
@@ -753,7 +763,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
     // lane 0 claims units and issues the TMA loads; in a flow launch the whole warp
     // first waits for the unit's dependencies (one completion tag per lane)
     uint64_t cpolicy = 0;
-    if constexpr (CPOL_ == 1)
+    if constexpr ((CPOL_ & 1) != 0)
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(cpolicy));
     uint32_t sp = 0, sc = 0;
     Unit s{0, 0, 0, 0};
@@ -815,7 +825,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
           if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
           mbar_expect_tx(&cfull[slot], NCOEF * T::kCExtBytes);
           for (int c = 0; c < NCOEF; ++c) {
-            if constexpr (CPOL_ == 1)
+            if constexpr ((CPOL_ & 1) != 0)
               tma_load_3d_hint(cring + slot * T::kCSlot + c * T::kCExtBytes, &maps.coef[c],
                                &cfull[slot], k0 - 4, j0 - 1, m, cpolicy);
             else
@@ -829,7 +839,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
     }
   } else if (warp < NW1) {
     // ------------------------------------- step-1 warps (tile row r = j0-1+r)
-    const int r = warp * RPW + half;
+    const int r = XS ? (warp < NW1 - 1 ? 2 * warp + 1 + half : (half ? R1 - 1 : 0)) : warp * RPW + half;
+    [[maybe_unused]] const uint32_t xs_tl =
+        tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * (kXSlots * 48));
     uint32_t sc = 0, sq = 0;
     int pslot = 0;          // p0 ring position, advanced incrementally (SP = 3 is not a
     uint32_t pphase = 0;    // power of two: no division per plane)
@@ -883,6 +895,51 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         // recomputes the neighbours' adjacent planes (two-plane halos)
         const bool plane_in = m >= g_lo && m < g_hi;
         float v[4];
+        if constexpr (XS) {
+          // p1 ring slot and stash slot of this plane free (qempty: step 2 finished the
+          // iteration that read the stash slot's previous plane), then the quads: shared
+          // memory -> registers -> tensor memory (planes that carry an output plane)
+          const int qslot = sq % SQ;
+          if (sq >= (uint32_t)SQ) mbar_wait(&qempty[qslot], ((sq / SQ) - 1) & 1);
+          tmem_fence_after();
+          float cv[48];
+#pragma unroll
+          for (int c = 0; c < NCOEF; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(ct + c * (QK * R1));
+            cv[4 * c] = q.x; cv[4 * c + 1] = q.y; cv[4 * c + 2] = q.z; cv[4 * c + 3] = q.w;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&cempty[cslot]);
+          if (warp < NW1 - 1 && m >= ia && m < ib) {
+            const uint32_t ta = xs_tl + (uint32_t)((sc % kXSlots) * 48);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              float t16[16];
+#pragma unroll
+              for (int x = 0; x < 16; ++x) t16[x] = cv[16 * k + x];
+              tmem_st16(ta + 16 * k, t16);
+            }
+          }
+          if (plane_in && row_in) {
+            auto Q = [&](int c) {
+              return make_float4(cv[4 * c], cv[4 * c + 1], cv[4 * c + 2], cv[4 * c + 3]);
+            };
+            float ss[4];
+            ss_quad2q(Q, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) v[x] = in1[x] ? fadd(el(b0.v, x), fmul(omega, ss[x])) : el(b0.v, x);
+          } else {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) v[x] = el(b0.v, x);
+          }
+          ++sc;
+          float* q1 = p1ring + qslot * (QK * R1);
+          *reinterpret_cast<float4*>(q1 + r * QK + hl * 4) = make_float4(v[0], v[1], v[2], v[3]);
+          tmem_wait_st();
+          tmem_fence_before();
+          mbar_arrive(&qfull[qslot]);   // release: this thread's p1 quad and stash quads
+          ++sq;
+        } else {
         if (plane_in && row_in) {
           float ss[4];
           ss_quad2<QK * R1>(ct, am, a0, ap, bm, b0, bp, cm, c0, cp, ss);
@@ -902,6 +959,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         *reinterpret_cast<float4*>(q1 + r * QK + hl * 4) = make_float4(v[0], v[1], v[2], v[3]);
         mbar_arrive(&qfull[qslot]);   // release: publishes this thread's quad
         ++sq;
+        }
         am = bm; a0 = b0; ap = bp;
         bm = cm; b0 = c0; bp = cp;
       }
@@ -914,7 +972,8 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
     // only while step 1 works on it, and the producer runs a plane further ahead.
     const int w2 = warp - NW1;
     const int r2 = w2 * RPW + half;
-    const uint32_t tl = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((w2 >> 2) * 96);
+    const uint32_t tl = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) +
+                        (uint32_t)((w2 >> 2) * (XS ? kXSlots * 48 : 96));
     uint32_t sc = 0, sq = 0;
     Unit s;
     for (uint32_t n = 0;; ++n) {
@@ -935,6 +994,58 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
       Row ym, y0, yp, zm, z0, zp;   // p1 queue: planes m-2 (y*), m-1 (z*)
 #pragma unroll 1
       for (int m = ia - 1; m <= ib; ++m) {
+        if constexpr (XS) {
+          // the stash of plane m-1 was written by step-1 warp w2 (same lanes) before it
+          // released p1(m-1); read it with p1(m), then release the p1 slot
+          const int qslot = sq % SQ;
+          mbar_wait(&qfull[qslot], (sq / SQ) & 1);
+          tmem_fence_after();
+          const float* q1 = p1ring + qslot * (QK * R1);
+          const Row nm = load_row1<LW>(q1, r2, hl), n0 = load_row1<LW>(q1, r2 + 1, hl),
+                    np = load_row1<LW>(q1, r2 + 2, hl);
+          float cv[48];
+          if (m >= ia + 1) {
+            const uint32_t ta = tl + (uint32_t)(((sc - 1) % kXSlots) * 48);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              float v[16];
+              tmem_ld16(ta + 16 * k, v);
+#pragma unroll
+              for (int x = 0; x < 16; ++x) cv[16 * k + x] = v[x];
+            }
+            tmem_wait_ld24(cv);
+            tmem_wait_ld24(cv + 24);
+          }
+          tmem_fence_before();
+          mbar_arrive(&qempty[qslot]);
+          ++sq;
+          ++sc;
+          if (m >= ia + 1) {
+            auto Q = [&](int c) {
+              return make_float4(cv[4 * c], cv[4 * c + 1], cv[4 * c + 2], cv[4 * c + 3]);
+            };
+            float ss[4];
+            ss_quad2q(Q, ym, y0, yp, zm, z0, zp, nm, n0, np, ss);
+            float w[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              w[x] = fadd(el(z0.v, x), fmul(omega, ss[x]));
+              if (writer && in2[x]) acc += (double)fmul(ss[x], ss[x]);
+            }
+            if (writer) {
+              float* o = ((pass & 1) ? fl.out[1] : fl.out[0]) + F.at(m - 1, j, kq);
+              if (in2[0] && in2[1] && in2[2] && in2[3]) {
+                *reinterpret_cast<float4*>(o) = make_float4(w[0], w[1], w[2], w[3]);
+              } else {
+                for (int x = 0; x < 4; ++x)
+                  if (in2[x]) o[x] = w[x];
+              }
+            }
+          }
+          ym = zm; y0 = z0; yp = zp;
+          zm = nm; z0 = n0; zp = np;
+          continue;
+        }
         {
           const int cslot = sc % SC;
           mbar_wait(&cfull[cslot], (sc / SC) & 1);
@@ -1275,6 +1386,8 @@ const void* smem_kernel(int id) {
     case 7: return (const void*)k_stencil_tb2<16, 8, 4, true>;
     case 8: return (const void*)k_stencil_tx<kTxTJ>;
     case 9: return (const void*)k_stencil_tb2<16, 8, 4, true, 1>;
+    case 10: return (const void*)k_stencil_tb2<16, 8, 4, true, 4>;
+    case 11: return (const void*)k_stencil_tb2<16, 8, 4, true, 5>;
     default: return nullptr;
   }
 }
@@ -1666,6 +1779,15 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
   switch (v) {
     case 1:
       if (env_int("HIMENO_TB2_STASH") != 0) {
+        // cross-warp stash (default; HIMENO_TB2_XS=0: each step-2 warp copies its own
+        // quads from shared memory): L -1.6..3.6 %, M -2.5 %, XL -1.5..3.6 % per pass
+        if (env_int("HIMENO_TB2_XS") != 0) {
+          if (passes > 1 && env_int("HIMENO_FLOW_CPOL") != 0)
+            return launch_tb2<16, 8, 4, true, 5>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                                 g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
+          return launch_tb2<16, 8, 4, true, 4>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                               g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
+        }
         if (passes > 1 && env_int("HIMENO_FLOW_CPOL") != 0)
           return launch_tb2<16, 8, 4, true, 1>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
                                                g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);

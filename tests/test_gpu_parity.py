@@ -436,7 +436,7 @@ def test_smem_optin_raised_on_every_device_used(gpu):
             ctx.init_device()
             ctx.jacobi_device(3, 1)
             ctx.sync()
-            assert N.smem_optin(7, dev) > 48 * 1024, dev   # two-step kernel, stash
+            assert N.smem_optin(10, dev) > 48 * 1024, dev  # two-step kernel, cross-warp stash
             assert N.smem_optin(1, dev) > 48 * 1024, dev   # single-step, 3 stages
 
 
@@ -754,5 +754,33 @@ def test_trimmed_tma_extents_bit_exact(gpu, monkeypatch, dims, kernel, trim):
         assert used == "k_stencil_tx"
     elif kernel == "tb2":
         assert used.startswith("k_stencil_tb2")
+    assert np.array_equal(p, ref["fields"]["p"])
+    assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"HIMENO_TB2_XS": "0"}, {"HIMENO_TB2_XS": "1"},
+                                 {"HIMENO_TB2_STASH": "0"},
+                                 {"HIMENO_TB2_XS": "0", "HIMENO_TB2_FLOW": "1"},
+                                 {"HIMENO_TB2_XS": "1", "HIMENO_TB2_FLOW": "1"}])
+@pytest.mark.parametrize("dims,nn", [((75, 45, 141), 6), ((129, 129, 257), 5)])
+def test_two_step_stash_variants_bit_exact(gpu, monkeypatch, dims, nn, env):
+    """Step-2 coefficients from the cross-warp stash (step-1 warps write the quads they
+    loaded into tensor memory; default), from each step-2 warp's own copy, or straight
+    from shared memory: the oracle's field bit for bit, per-pass and flow launches."""
+    sz = himeno.custom_size(*dims)
+    ref = oracle.run_program(sz.I, sz.J, sz.K, nn)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    lib = N.load()
+    old = lib.hp_set_temporal_blocking(1)
+    try:
+        with N.Context(0, sz.I, sz.J, sz.K) as ctx:
+            ctx.init_device()
+            ctx.jacobi_device(nn, 1)
+            assert N.last_two_step_kernel().startswith("k_stencil_tb2")
+            p, g = ctx.read_field("p", 1), ctx.read_gosa(1)
+    finally:
+        lib.hp_set_temporal_blocking(old)
     assert np.array_equal(p, ref["fields"]["p"])
     assert abs(g - ref["gosa64"]) <= GOSA_RTOL * ref["gosa64"]

@@ -27,8 +27,31 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Bounded wait: a pipeline bug must abort the kernel (trap -> launch error),
 // never hang the GPU.  2^26 polls (each try_wait suspends up to a
 // hardware-defined interval) is seconds, far beyond any legitimate wait.
+// try_wait suspend-time hint (ns) of mbar_wait: 1000 -> M flow pass 42.4 -> 40.3 us, L
+// pass -1..2 %: the polling loops of waiting warps had been ~19 % of the two-step kernel's
+// executed instructions (profiles/r02_tb2_experiments_late.md).  0 = no hint.
+#ifndef HP_MBAR_HINT_NS
+#define HP_MBAR_HINT_NS 1000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
+#if HP_MBAR_HINT_NS > 0
+  // suspend-time hint: a waiting warp sleeps until the phase completes (or the hint
+  // expires) instead of re-polling, leaving its issue slots to the working warps
+#pragma unroll 1
+  for (uint32_t n = 0; n < (1u << 26) / (HP_MBAR_HINT_NS / 100 + 1) + 16; ++n) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)HP_MBAR_HINT_NS)
+        : "memory");
+    if (done) return;
+  }
+#else
 #pragma unroll 1
   for (uint32_t n = 0; n < (1u << 26); ++n) {
     asm volatile(
@@ -42,6 +65,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
   }
+#endif
   asm volatile("trap;");
 }
 // try_wait with a short suspend hint (ns): true once the phase has completed

@@ -726,6 +726,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   // 15), so step-2 warp w2 needs exactly step-1 warp w2's quads, in the same TMEM lanes
   // (warps 8+w2 and w2 share the lane quarter w2 % 4).  Five stash slots per plane ring.
   constexpr bool XS = (CPOL_ & 4) != 0;
+  constexpr bool LATE_P = XS && (CPOL_ & 1) != 0;
   constexpr uint32_t kStashCols = XS ? 512 : 256;
   constexpr int kXSlots = 5;
   static_assert(!ST_ || (NW1 % 4 == 0 && NW2 <= 8), "stash: (warp%4, block) per step-2 warp");
@@ -885,8 +886,15 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         const float* pt = reinterpret_cast<const float*>(p0ring + cur * T::kP0Slot);
         const Row cm = load_row0<LW>(pt, r, hl), c0 = load_row0<LW>(pt, r + 1, hl),
                   cp = load_row0<LW>(pt, r + 2, hl);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[cur]);
+        // flow launches (XS with evict_first): the p0 slot is released together with the
+        // coefficient stage, after both stages' loads are in flight (M -2.4 % per pass);
+        // per-pass launches release it here, so the producer -- which issues p0(m+1)
+        // before the coefficients of plane m -- is not held behind the cfull wait (XL +1.2 %
+        // with the late release)
+        if constexpr (!LATE_P) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pempty[cur]);
+        }
         next_p();
         const int cslot = sc % SC;
         mbar_wait(&cfull[cslot], (sc / SC) & 1);
@@ -909,7 +917,10 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
             cv[4 * c] = q.x; cv[4 * c + 1] = q.y; cv[4 * c + 2] = q.z; cv[4 * c + 3] = q.w;
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&cempty[cslot]);
+          if (lane == 0) {
+            if constexpr (LATE_P) mbar_arrive(&pempty[cur]);
+            mbar_arrive(&cempty[cslot]);
+          }
           if (warp < NW1 - 1 && m >= ia && m < ib) {
             const uint32_t ta = xs_tl + (uint32_t)((sc % kXSlots) * 48);
 #pragma unroll

@@ -264,7 +264,9 @@ int hp_dd_time_steps(hp_ctx* ctx, int steps, int nn, double* ms_out);
  * kernel `id` has in `device`'s context (0..2 single-step stencil with 2..4
  * stages, 3..6 two-step shapes, 7 two-step with the tensor-memory stash, 8 the
  * two-step tile-exchange kernel, 9 kernel 7 with evict_first coefficient loads, used
- * by flow launches, 10 / 11 kernels 7 / 9 with the cross-warp stash -- the defaults).  The library raises it per device before the
+ * by flow launches, 10 kernel 7 with the cross-warp stash, 11 kernel 10 for flow launches
+ * (evict_first, coefficients-first order), 12 kernel 10 with the coefficients-first order
+ * -- 10 / 11 / 12 are the defaults).  The library raises it per device before the
  * first launch there. */
 int hp_smem_optin(int id, int device, int* bytes);
 /* Diagnostics: the kernel the most recent two-step launch (any context) used:

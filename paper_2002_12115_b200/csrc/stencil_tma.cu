@@ -726,7 +726,13 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
   // 15), so step-2 warp w2 needs exactly step-1 warp w2's quads, in the same TMEM lanes
   // (warps 8+w2 and w2 share the lane quarter w2 % 4).  Five stash slots per plane ring.
   constexpr bool XS = (CPOL_ & 4) != 0;
-  constexpr bool LATE_P = XS && (CPOL_ & 1) != 0;
+  // CPOL_ & 8 (with XS): the producer issues plane m's coefficients before p0(m+1) and
+  // step 1 releases the p0 slot together with the coefficient stage, after both loads
+  // are in flight (one load-latency stall less per plane).  It lets the columns drift
+  // further apart, so it is used where L2 holds many planes (M, L), not on XL
+  // (profiles/r02_tb2_experiments_late.md).
+  constexpr bool ORD = XS && (CPOL_ & 8) != 0;
+  constexpr bool LATE_P = ORD;
   constexpr uint32_t kStashCols = XS ? 512 : 256;
   constexpr int kXSlots = 5;
   static_assert(!ST_ || (NW1 % 4 == 0 && NW2 <= 8), "stash: (warp%4, block) per step-2 warp");
@@ -821,7 +827,7 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
         load_p0(ia - 2);
         load_p0(ia - 1);
         for (int m = ia - 1; m <= ib; ++m) {
-          load_p0(m + 1);
+          if constexpr (!ORD) load_p0(m + 1);
           const int slot = sc % SC;
           if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
           mbar_expect_tx(&cfull[slot], NCOEF * T::kCExtBytes);
@@ -834,6 +840,9 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
                           k0 - 4, j0 - 1, m);
           }
           ++sc;
+          // ORD: plane m's coefficients go out before p0(m+1), so a p0 slot still held
+          // by step 1 (released with the coefficient stage) delays only the next p0 box
+          if constexpr (ORD) load_p0(m + 1);
         }
       }
       __syncwarp();
@@ -1398,7 +1407,8 @@ const void* smem_kernel(int id) {
     case 8: return (const void*)k_stencil_tx<kTxTJ>;
     case 9: return (const void*)k_stencil_tb2<16, 8, 4, true, 1>;
     case 10: return (const void*)k_stencil_tb2<16, 8, 4, true, 4>;
-    case 11: return (const void*)k_stencil_tb2<16, 8, 4, true, 5>;
+    case 11: return (const void*)k_stencil_tb2<16, 8, 4, true, 13>;
+    case 12: return (const void*)k_stencil_tb2<16, 8, 4, true, 12>;
     default: return nullptr;
   }
 }
@@ -1724,6 +1734,23 @@ int tx_error(const void* h) {
   return v ? 1 : 0;
 }
 
+// Coefficients-first producer order with late p0 release (CPOL_ & 8) for one-pass
+// launches: when L2 holds at least 8 planes of the 14 arrays (L: 17, XL: 4).  With it XL
+// read 22 % more DRAM (halo lines evicted between neighbouring columns); L runs 3 %
+// faster.  HIMENO_TB2_ORD=0/1 forces it.
+static bool tb2_ord(const DevFields& F) {
+  const int force = env_int("HIMENO_TB2_ORD");
+  if (force >= 0) return force != 0;
+  int dev = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const double plane = 14.0 * F.J * F.P * 4.0;
+  return l2 >= 8.0 * plane;
+}
+
 // `passes` two-step passes p_in -> p_out -> p_in ... (2 * passes Jacobi iterations)
 // in one launch; the result is in p_out for an odd number of passes, p_in for an
 // even one.  Returns 1, 0 (not applicable: the caller runs single steps), or -1.
@@ -1794,8 +1821,11 @@ static int launch_two_step(const DevFields& F, const void* h, const float* p_in,
         // quads from shared memory): L -1.6..3.6 %, M -2.5 %, XL -1.5..3.6 % per pass
         if (env_int("HIMENO_TB2_XS") != 0) {
           if (passes > 1 && env_int("HIMENO_FLOW_CPOL") != 0)
-            return launch_tb2<16, 8, 4, true, 5>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
-                                                 g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
+            return launch_tb2<16, 8, 4, true, 13>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                                  g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
+          if (tb2_ord(F))
+            return launch_tb2<16, 8, 4, true, 12>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
+                                                  g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
           return launch_tb2<16, 8, 4, true, 4>(maps, F, fl, i_lo, i_hi, j_lo, j_hi, k_lo, k_hi,
                                                g_lo, g_hi, c.chunk, c.full, a, g, s, sms, r2);
         }

@@ -436,7 +436,8 @@ def test_smem_optin_raised_on_every_device_used(gpu):
             ctx.init_device()
             ctx.jacobi_device(3, 1)
             ctx.sync()
-            assert N.smem_optin(10, dev) > 48 * 1024, dev  # two-step kernel, cross-warp stash
+            # two-step kernel (cross-warp stash, coefficients-first order: M's planes fit L2)
+            assert N.smem_optin(12, dev) > 48 * 1024, dev
             assert N.smem_optin(1, dev) > 48 * 1024, dev   # single-step, 3 stages
 
 

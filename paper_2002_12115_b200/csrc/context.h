@@ -39,6 +39,11 @@ struct hp_ctx {
   uint64_t launches = 0;         // kernels launched by this context (all entry points)
   double* pending_gosa = nullptr;  // hp_jacobi_host_async: where hp_sync delivers gosa
   cudaEvent_t h2d_done = nullptr;  // end of this context's last host-input upload
+  // hp_jacobi_host uploads: copy stream + second staging buffer, so the H2D copy of one
+  // field overlaps the on-device repitch of the previous one (created on first use)
+  cudaStream_t up = nullptr;
+  float* stage2 = nullptr;
+  cudaEvent_t up_start = nullptr, up_ev[2] = {}, rep_ev[2] = {};
   // slab decomposition (decomp.cpp): this context holds global planes
   // [i_off, i_off + I) of a gI-plane grid; stencil interior = local [li_lo, li_hi)
   int gI = 0, i_off = 0, li_lo = 1, li_hi = 0;

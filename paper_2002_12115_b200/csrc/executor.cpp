@@ -211,6 +211,13 @@ extern "C" void hp_destroy(hp_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   forget_upload(c);
   if (c->h2d_done) cudaEventDestroy(c->h2d_done);
+  if (c->up) {
+    cudaStreamSynchronize(c->up);
+    cudaStreamDestroy(c->up);
+  }
+  for (cudaEvent_t e : {c->up_start, c->up_ev[0], c->up_ev[1], c->rep_ev[0], c->rep_ev[1]})
+    if (e) cudaEventDestroy(e);
+  if (c->stage2) cudaFree(c->stage2);
   if (c->dd) dd_destroy(c);
   if (c->dev.tma) destroy_stencil_tma(const_cast<void*>(c->dev.tma));
   if (c->slab) cudaFree(c->slab);
@@ -1296,14 +1303,41 @@ static int jacobi_host_enqueue(hp_ctx* c, const float* const* fields, int nn, in
   }
   if (!c->h2d_done)
     CK(cudaEventCreateWithFlags(&c->h2d_done, cudaEventDisableTiming), "cudaEventCreate");
+  if (!c->up) {
+    // copy stream, events and the second staging buffer of the double-buffered upload
+    CK(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (cudaEvent_t* e : {&c->up_start, &c->up_ev[0], &c->up_ev[1], &c->rep_ev[0], &c->rep_ev[1]})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    CK(cudaMalloc(&c->stage2, (size_t)c->I * c->J * c->K * sizeof(float)), "cudaMalloc stage");
+  }
   {
+    // H2D of field i into staging buffer i % 2 on the copy stream, repitch into the
+    // field on the compute stream: the link moves field i+1 while field i is repitched
+    // (one buffer: the link idled ~0.1 ms per field on L)
     std::lock_guard<std::mutex> lock(g_upload_mu);
     const bool tok = c->device >= 0 && c->device < 64;
+    CK(cudaEventRecord(c->up_start, c->stream), "upload start");   // staging buffers free
+    CK(cudaStreamWaitEvent(c->up, c->up_start, 0), "upload start");
     if (tok && g_last_upload[c->device])
-      CK(cudaStreamWaitEvent(c->stream, g_last_upload[c->device], 0), "upload order");
-    for (int f = 0; f < HP_NFIELDS; ++f)
-      if (f != HP_F_WRK2) CK(field_to_device(c, c->dev.f[f], fields[f]), "jacobi H2D");
-    CK(cudaEventRecord(c->h2d_done, c->stream), "upload event");
+      CK(cudaStreamWaitEvent(c->up, g_last_upload[c->device], 0), "upload order");
+    float* stage[2] = {c->scratch, c->stage2};
+    const size_t n = (size_t)c->I * c->J * c->K;
+    int i = 0;
+    for (int f = 0; f < HP_NFIELDS; ++f) {
+      if (f == HP_F_WRK2) continue;
+      const int b = i & 1;
+      if (i >= 2) CK(cudaStreamWaitEvent(c->up, c->rep_ev[b], 0), "stage reuse");
+      CK(cudaMemcpyAsync(stage[b], fields[f], n * sizeof(float), cudaMemcpyHostToDevice, c->up),
+         "jacobi H2D");
+      CK(cudaEventRecord(c->up_ev[b], c->up), "H2D event");
+      CK(cudaStreamWaitEvent(c->stream, c->up_ev[b], 0), "H2D wait");
+      if (launch_repitch(c->dev.f[f], (size_t)c->P, stage[b], (size_t)c->K, c->K,
+                         (size_t)c->I * c->J, c->stream) < 0)
+        CK(cudaGetLastError(), "repitch");
+      CK(cudaEventRecord(c->rep_ev[b], c->stream), "repitch event");
+      ++i;
+    }
+    CK(cudaEventRecord(c->h2d_done, c->up), "upload event");
     if (tok) g_last_upload[c->device] = c->h2d_done;
   }
   int rc = hp_jacobi_device(c, nn, variant);

@@ -691,11 +691,14 @@ __device__ __forceinline__ void boundary_signal(const Flow& fl, bool boundary, i
   }
 }
 
-// CPOL_ = 1: the coefficient TMA loads carry an L2 evict_first policy.  The flow launch
-// (several passes in flight, small grids) runs 2.7 % faster with it on M; on L, whose
-// step-1 halo lines must survive in L2 until the neighbouring tile reads them, it costs
-// 28 % (profiles/r02_flow.md), so per-pass launches keep CPOL_ = 0 (no hint at all: an
-// evict_normal hint already costs 0.7 %).
+// CPOL_ is a bit set of variants (instantiations: 0, 1, 4, 12, 13):
+//   1  the coefficient TMA loads carry an L2 evict_first policy.  The flow launch
+//      (several passes in flight, small grids) runs 2.7 % faster with it on M; on L, whose
+//      step-1 halo lines must survive in L2 until the neighbouring tile reads them, it
+//      costs 28 % (profiles/r02_flow.md), so per-pass launches go without (no hint at
+//      all: an evict_normal hint already costs 0.7 %).
+//   4  cross-warp stash (XS, below): step 1 hands the step-2 coefficients over in TMEM.
+//   8  (with 4) coefficients-first producer order and late p0 release (ORD, below).
 template <int LW, int NW1_, int SC_, bool ST_ = false, int CPOL_ = 0>
 __global__ void __launch_bounds__(Tb2<LW, NW1_, SC_>::kThreads, 1)
 k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i_hi, int j_lo,

@@ -1744,11 +1744,16 @@ int tx_error(const void* h) {
 static bool tb2_ord(const DevFields& F) {
   const int force = env_int("HIMENO_TB2_ORD");
   if (force >= 0) return force != 0;
-  int dev = 0, l2 = 0;
+  static std::atomic<int> l2_of[64] = {};   // L2 bytes per device (0: not queried yet)
+  int dev = 0;
   cudaGetDevice(&dev);
-  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+  int l2 = dev >= 0 && dev < 64 ? l2_of[dev].load() : 0;
+  if (l2 == 0) {
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (dev >= 0 && dev < 64) l2_of[dev] = l2;
   }
   const double plane = 14.0 * F.J * F.P * 4.0;
   return l2 >= 8.0 * plane;

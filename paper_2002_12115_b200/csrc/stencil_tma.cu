@@ -833,6 +833,15 @@ k_stencil_tb2(const __grid_constant__ Tb2Maps maps, DevFields F, int i_lo, int i
           if constexpr (!ORD) load_p0(m + 1);
           const int slot = sc % SC;
           if (sc >= (uint32_t)SC) mbar_wait(&cempty[slot], ((sc / SC) - 1) & 1);
+          if ((CPOL_ & 1) == 0 && (m < g_lo || m >= g_hi)) {
+            // one-pass launches: a plane outside the global interior carries no data (step
+            // 1 computes nothing there, step 2 has no output plane); a plain arrive
+            // completes the stage
+            ++sc;
+            mbar_arrive(&cfull[slot]);
+            if constexpr (ORD) load_p0(m + 1);
+            continue;
+          }
           mbar_expect_tx(&cfull[slot], NCOEF * T::kCExtBytes);
           for (int c = 0; c < NCOEF; ++c) {
             if constexpr ((CPOL_ & 1) != 0)

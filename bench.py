@@ -545,6 +545,15 @@ def run_ours(args, world, rank, local):
                 "launch_ms": kt.stencil_ms, "share_of_step": kt.stencil_ms * kt.n_stencil / kt.total_ms,
                 "iterations_per_launch": kt.stencil_iters,
                 "peak_source": peak_src}
+    # the same kernel inside the timed region: its launches run back to back there (PDL
+    # overlaps each launch's tail with the next one's start, which per-launch events
+    # prevent); the whole step's device time is charged to the stencil launches, so this
+    # is a lower bound for the in-step rate
+    if kt.n_stencil > 0 and ms_max > 0:
+        in_step_ms = ms_max / args.steps / kt.n_stencil
+        in_step = launch_bytes(points, kt.stencil_iters) / (in_step_ms / 1e3) / 1e9
+        roofline["in_step"] = {"launch_ms": in_step_ms, "achieved": in_step, "frac": in_step / peak,
+                               "launches_per_step": kt.n_stencil}
     # the same box's device-to-device copy bandwidth, measured now (context for `peak`)
     try:
         live = copy_bandwidth_gbs(local)

@@ -42,6 +42,26 @@ del os.environ["HIMENO_TB2_FLOW"], os.environ["HIMENO_FLOW_CHUNK"]
 os.environ["HIMENO_DD_OVERLAP"] = "1"
 with dd.GroupJacobi("XS", [0, 0, 0]) as g:
     print("group overlapped", g.jacobi(4))
+# the two-step variants the small grid does not pick by default (old producer order,
+# per-warp stash), and the double-buffered host upload of hp_jacobi_host (serial and two
+# contexts in flight)
+import numpy as np  # noqa: E402
+for env in ({"HIMENO_TB2_ORD": "0"}, {"HIMENO_TB2_XS": "0"}):
+    os.environ.update(env)
+    with N.Context(0, sz.I, sz.J, sz.K) as c:
+        c.init_device()
+        c.jacobi_device(3, 1)
+        print("variant", env, c.read_gosa(1))
+    for k in env:
+        del os.environ[k]
+with N.Context(0, sz.I, sz.J, sz.K) as a, N.Context(0, sz.I, sz.J, sz.K) as b:
+    a.init_device()
+    host = {f: a.read_field(f, 1) for f in N.FIELDS}
+    outs = [np.empty_like(host["p"]), np.empty_like(host["p"])]
+    print("host serial", a.jacobi_host(host, 3, 1, outs[0]))
+    a.jacobi_host_async(host, 3, 1, outs[0])
+    b.jacobi_host_async(host, 3, 1, outs[1])
+    print("host async", a.sync(), b.sync())
 if os.environ.get("SANITIZE_TX") == "1":
     os.environ["HIMENO_TX"] = "2"
     with N.Context(0, sz.I, sz.J, sz.K) as c:
